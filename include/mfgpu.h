@@ -1,0 +1,97 @@
+/* mfgpu.h — C-ABI of the B200 scoring engine (libmfgpu.so).
+ *
+ * Drop-in seam: this library replaces the reference's
+ *   ScoringModel(container, compute_mode)        pkg/src/metricforge/encoder.py:94-118
+ *   ScoringModel.score_records(encoded_records)  pkg/src/metricforge/encoder.py:214-226
+ * i.e. everything from padded token ids to one float32 score per record
+ * (forward, BOS pool, per-kind features, regression head). Its four-call
+ * shape (create / score / last_error / destroy) mirrors the flat boundary the
+ * reference exposes to other languages in pkg/frontend/src/boundary.ts:185-261
+ * (create / evaluateBatch / lastError / destroy).
+ *
+ * Ownership: all host buffers are caller-owned and only read/written during
+ * the call. The context owns device weights and workspaces. One caller thread
+ * per context at a time (the Python wrapper serialises, like Evaluator's lock,
+ * pkg/src/metricforge/evaluate.py:159,182).
+ *
+ * Return codes (mirroring the CLI's exit-code split, pkg/src/metricforge/cli.py:40-47):
+ *   MFG_OK 0, MFG_ERR_RUNTIME 1 (CUDA / I/O), MFG_ERR_USAGE 2 (bad ids, lengths,
+ *   arguments), MFG_ERR_CONTAINER 3 (format, missing or mis-shaped tensor).
+ */
+#ifndef MFGPU_H
+#define MFGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MFG_OK 0
+#define MFG_ERR_RUNTIME 1
+#define MFG_ERR_USAGE 2
+#define MFG_ERR_CONTAINER 3
+
+/* Arithmetic of the encoder/head GEMMs. */
+#define MFG_PREC_FP32 0 /* fp32-parity: bf16x3 split operands on tcgen05 (|d| <= 1e-3 vs fp32 ref) */
+#define MFG_PREC_BF16 1 /* single bf16 MMA per k-step, fp32 accumulate (reported separately) */
+
+typedef struct mfg_ctx mfg_ctx;
+
+typedef struct {
+  const char* container_path; /* .mfrg file (pkg/src/metricforge/container.py layout) */
+  int32_t device;             /* CUDA ordinal */
+  int32_t precision;          /* MFG_PREC_* */
+  int64_t max_tokens;         /* workspace capacity per device chunk (0 = default 262144) */
+  int32_t max_records;        /* records per device chunk (0 = default 4096) */
+  int32_t profile;            /* 1 = time every launch with CUDA events (see mfg_stats) */
+} mfg_config;
+
+/* Maps the container, checks the tensor-name/shape contract of
+ * required_tensor_shapes (encoder.py:69-91), uploads and pre-splits weights. */
+int mfg_create(const mfg_config* cfg, mfg_ctx** out);
+
+/* Score n_records records of n_roles token sequences each.
+ *   ids:        all sequences concatenated ROLE-MAJOR: role 0 of records 0..n-1,
+ *               then role 1 of records 0..n-1, ...; values in [0, vocab_size)
+ *   cu_seqlens: [n_roles * n_records + 1] offsets into ids (cu_seqlens[0] == 0)
+ *   scores_out: [n_records] float32, same record order
+ * Roles follow SEGMENT_ROLES (encoder.py:40-44): comet-qe (src, mt),
+ * comet (src, mt, ref), bleurt (joint). */
+int mfg_score_batch(mfg_ctx* ctx, int32_t n_records, int32_t n_roles, const int32_t* ids,
+                    const int64_t* cu_seqlens, float* scores_out);
+
+/* Error of the last failing call on ctx (ctx == NULL: last mfg_create / test
+ * call on this thread). Copies a NUL-terminated message into buf. */
+int mfg_last_error(const mfg_ctx* ctx, int32_t* code, char* buf, size_t cap);
+
+void mfg_destroy(mfg_ctx* ctx);
+
+/* ---- introspection ------------------------------------------------------ */
+typedef struct {
+  int32_t kind; /* 0 comet-qe, 1 comet, 2 bleurt */
+  int32_t vocab_size, d_model, n_heads, n_layers, d_ffn, max_position, pre_norm;
+  int32_t n_roles, n_head_stages, precision, num_sms;
+  int64_t device_bytes; /* weights + workspaces resident on the device */
+} mfg_model_info;
+int mfg_get_model_info(const mfg_ctx* ctx, mfg_model_info* out);
+
+#define MFG_NCLASS 8 /* qkv, o_proj, ffn1, ffn2, attention, layernorm, embed, head */
+typedef struct {
+  double device_ms;        /* sum over calls of first-H2D..last-D2H event time */
+  int64_t calls, records, tokens, chunks;
+  int64_t kernel_launches; /* kernels this library launched */
+  /* per class (profile=1 only): event-timed ms, launches, algorithmic work */
+  double class_ms[MFG_NCLASS];
+  int64_t class_launches[MFG_NCLASS];
+  double class_flops[MFG_NCLASS]; /* algorithmic FLOPs (real, unpadded dims) */
+  double class_bytes[MFG_NCLASS]; /* algorithmic HBM bytes */
+} mfg_stats;
+int mfg_get_stats(const mfg_ctx* ctx, mfg_stats* out);
+int mfg_reset_stats(mfg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MFGPU_H */

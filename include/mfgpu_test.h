@@ -1,0 +1,32 @@
+/* mfgpu_test.h — kernel-level entry points of libmfgpu.so used by the parity
+ * tests (tests/test_gpu_kernels.py). Each call allocates its own device
+ * buffers on the current device, runs ONE production kernel and copies the
+ * result back; split (hi/lo) outputs are returned recombined as hi + lo.
+ * Not part of the scoring API. Return codes as in mfgpu.h. */
+#ifndef MFGPU_TEST_H
+#define MFGPU_TEST_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* out[M][N] = epilogue(A[M][K] · W[K][N] + bias[N] (+ residual[M][N])) through the
+ * tcgen05 GEMM. epi: 0 f32, 1 f32+residual, 2 gelu (split out), 3 tanh (split out). */
+int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, int32_t K, const float* A,
+              const float* W, const float* bias, const float* residual, float* out);
+
+/* ctx[T][d] = attention of packed qkv[T][3d] (q | k | v per row), sequences given by
+ * cu[n_seq + 1], heads = n_heads, scale 1/sqrt(d/heads). */
+int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* cu, int32_t d,
+                   int32_t n_heads, const float* qkv, float* ctx_out);
+
+/* out[T][d] = LayerNorm(y) with gain g and bias b (eps 1e-5). */
+int mfgt_layernorm(int32_t T, int32_t d, const float* y, const float* g, const float* b,
+                   float* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,104 @@
+// Host side of the tcgen05 GEMM: tensor-map encoding (driver entry point, no
+// libcuda link dependency) and the template dispatch.
+#include <cstdio>
+#include <mutex>
+
+#include "gemm_tc.cuh"
+#include "kernels.h"
+
+namespace mfg {
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode_fn() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
+                    uint64_t ld_elems, uint32_t box_rows, char* err, size_t errcap) {
+  PFN_encodeTiled enc = get_encode_fn();
+  if (!enc) {
+    snprintf(err, errcap, "cuTensorMapEncodeTiled unavailable from the driver");
+    return false;
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(err, errcap, "cuTensorMapEncodeTiled failed (%d): rows=%llu cols=%llu ld=%llu box=%u",
+             (int)r, (unsigned long long)rows, (unsigned long long)cols,
+             (unsigned long long)ld_elems, box_rows);
+    return false;
+  }
+  return true;
+}
+
+int gemm_pick_bn(int n_pad) {
+  if (n_pad % 256 == 0) return 256;
+  if (n_pad % 128 == 0) return 128;
+  return 64;
+}
+
+template <int BN, bool SPLIT, int EPI>
+static cudaError_t run(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* bh,
+                       const CUtensorMap* bl, const GemmArgs& a, int num_sms, cudaStream_t st) {
+  using C = GemmCfg<BN, SPLIT>;
+  auto kern = gemm_tc_kernel<BN, SPLIT, EPI>;
+  cudaError_t e =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const int tiles = ((a.M + GEMM_BM - 1) / GEMM_BM) * (a.N / BN);
+  if (tiles <= 0) return cudaSuccess;
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  kern<<<grid, GEMM_THREADS, C::SMEM_BYTES, st>>>(*ah, SPLIT ? *al : *ah, *bh, SPLIT ? *bl : *bh,
+                                                   a);
+  return cudaGetLastError();
+}
+
+template <int BN, bool SPLIT>
+static cudaError_t run_epi(int epi, const CUtensorMap* ah, const CUtensorMap* al,
+                           const CUtensorMap* bh, const CUtensorMap* bl, const GemmArgs& a,
+                           int num_sms, cudaStream_t st) {
+  switch (epi) {
+    case EPI_F32: return run<BN, SPLIT, EPI_F32>(ah, al, bh, bl, a, num_sms, st);
+    case EPI_F32_RES: return run<BN, SPLIT, EPI_F32_RES>(ah, al, bh, bl, a, num_sms, st);
+    case EPI_GELU_SPLIT: return run<BN, SPLIT, EPI_GELU_SPLIT>(ah, al, bh, bl, a, num_sms, st);
+    case EPI_TANH_SPLIT: return run<BN, SPLIT, EPI_TANH_SPLIT>(ah, al, bh, bl, a, num_sms, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_gemm(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* bh,
+                        const CUtensorMap* bl, int bn, bool split, int epi, const GemmArgs& a,
+                        int num_sms, cudaStream_t st) {
+  if (a.K % GEMM_BK != 0 || a.N % bn != 0) return cudaErrorInvalidValue;
+  if (split) {
+    if (bn == 256) return run_epi<256, true>(epi, ah, al, bh, bl, a, num_sms, st);
+    if (bn == 128) return run_epi<128, true>(epi, ah, al, bh, bl, a, num_sms, st);
+    if (bn == 64) return run_epi<64, true>(epi, ah, al, bh, bl, a, num_sms, st);
+  } else {
+    if (bn == 256) return run_epi<256, false>(epi, ah, al, bh, bl, a, num_sms, st);
+    if (bn == 128) return run_epi<128, false>(epi, ah, al, bh, bl, a, num_sms, st);
+    if (bn == 64) return run_epi<64, false>(epi, ah, al, bh, bl, a, num_sms, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace mfg

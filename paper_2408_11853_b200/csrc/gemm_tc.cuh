@@ -1,0 +1,240 @@
+// Persistent warp-specialised tcgen05 GEMM for sm_100a.
+//
+//   C[M, N] = A[M, K] · Bᵀ   with A row-major [M][K] and B stored [N][K]
+//   (weights are transposed once at load so both operands are K-major).
+//
+// Replaces the reference's `_mm`/`_affine` (`pkg/src/metricforge/encoder.py:120-126`)
+// and fuses the ops that follow each affine into the epilogue:
+//   EPI_F32        out = acc + bias                         (QKV, head output)
+//   EPI_F32_RES    out = acc + bias + residual              (O-proj, FFN2)
+//   EPI_GELU_SPLIT out = gelu_tanh(acc + bias) -> bf16 hi/lo (FFN1, `encoder.py:149-151`)
+//   EPI_TANH_SPLIT out = tanh(acc + bias)      -> bf16 hi/lo (head hidden stages, `:190-196`)
+//
+// SPLIT=true is the fp32-parity path ("bf16x3"): A = A_hi + A_lo and
+// B = B_hi + B_lo are bf16 pairs and every k-step issues
+//   D += A_hi·B_hi + A_lo·B_hi + A_hi·B_lo
+// into one fp32 TMEM accumulator (~16 mantissa bits per operand).
+// SPLIT=false is the plain bf16 path (one MMA per k-step).
+//
+// Roles (256 threads): warp0 lane0 = TMA producer, warp1 lane0 = MMA issuer,
+// warp2 = TMEM allocator, warps4-7 = epilogue (warp w owns TMEM lanes
+// 32*(w%4)..+31 = tile rows). Two TMEM accumulators let the epilogue of tile
+// i overlap the MMAs of tile i+1. Tiles are assigned round-robin to a
+// persistent grid of <= #SM CTAs.
+#pragma once
+#include "ptx.cuh"
+
+namespace mfg {
+
+enum EpiMode : int { EPI_F32 = 0, EPI_F32_RES = 1, EPI_GELU_SPLIT = 2, EPI_TANH_SPLIT = 3 };
+
+struct GemmArgs {
+  int M, N, K;               // M real rows; N, K padded (N % BN == 0, K % 64 == 0)
+  const float* bias;         // [N]
+  const float* residual;     // [M][ldr] (EPI_F32_RES)
+  int ldr;
+  float* out_f32;            // [M][ldo] (EPI_F32*)
+  int ldo;
+  __nv_bfloat16* out_hi;     // [M][ldh] (split epilogues)
+  __nv_bfloat16* out_lo;     // may be null when the consumer GEMM is not split
+  int ldh;
+};
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK = 64;
+constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_SMEM_LIMIT = 232448;  // 227 KB opt-in dynamic smem
+constexpr int GEMM_EPI_BYTES = 4 * 32 * 33 * 4;
+constexpr int GEMM_BAR_BYTES = 256;
+
+template <int BN, bool SPLIT>
+struct GemmCfg {
+  static constexpr int NOPS = SPLIT ? 2 : 1;
+  static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
+  static constexpr int B_BYTES = BN * GEMM_BK * 2;
+  static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
+  static constexpr int STAGES_FIT =
+      (GEMM_SMEM_LIMIT - 1024 - GEMM_EPI_BYTES - GEMM_BAR_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr int SMEM_BYTES =
+      1024 + STAGES * STAGE_BYTES + GEMM_EPI_BYTES + GEMM_BAR_BYTES;
+  static constexpr uint32_t TMEM_COLS =
+      2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  static_assert(STAGES >= 2, "pipeline needs at least two stages");
+  static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
+};
+
+template <int BN, bool SPLIT, int EPI>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap mapAh,
+                   const __grid_constant__ CUtensorMap mapAl,
+                   const __grid_constant__ CUtensorMap mapBh,
+                   const __grid_constant__ CUtensorMap mapBl, const GemmArgs args) {
+  using C = GemmCfg<BN, SPLIT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  float* epi_buf = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + GEMM_EPI_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapAh);
+    tma_prefetch(&mapBh);
+    if (SPLIT) {
+      tma_prefetch(&mapAl);
+      tma_prefetch(&mapBl);
+    }
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_m = (args.M + GEMM_BM - 1) / GEMM_BM;
+  const int num_n = args.N / BN;
+  const int tiles = num_m * num_n;
+  const int kblocks = args.K / GEMM_BK;
+
+  auto stage_ptr = [&](int s, int which) -> uint8_t* {
+    // which: 0 A_hi, 1 A_lo, 2 B_hi, 3 B_lo
+    uint8_t* base = smem + s * C::STAGE_BYTES;
+    if (which < 2) return base + which * C::A_BYTES;
+    return base + C::NOPS * C::A_BYTES + (which - 2) * C::B_BYTES;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m0 = (tile / num_n) * GEMM_BM;
+        const int n0 = (tile % num_n) * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          const int k0 = kb * GEMM_BK;
+          tma_load_2d(stage_ptr(stage, 0), &mapAh, &full[stage], k0, m0);
+          tma_load_2d(stage_ptr(stage, 2), &mapBh, &full[stage], k0, n0);
+          if (SPLIT) {
+            tma_load_2d(stage_ptr(stage, 1), &mapAl, &full[stage], k0, m0);
+            tma_load_2d(stage_ptr(stage, 3), &mapBl, &full[stage], k0, n0);
+          }
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ah = umma_desc_sw128(stage_ptr(stage, 0));
+          const uint64_t bh = umma_desc_sw128(stage_ptr(stage, 2));
+          const uint64_t al = SPLIT ? umma_desc_sw128(stage_ptr(stage, 1)) : 0;
+          const uint64_t bl = SPLIT ? umma_desc_sw128(stage_ptr(stage, 3)) : 0;
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k) {
+            const uint64_t adv = (uint64_t)(k * 32) >> 4;  // 16 bf16 along K
+            tc_mma_bf16(d, ah + adv, bh + adv, idesc, (kb | k) != 0);
+            if (SPLIT) {
+              tc_mma_bf16(d, al + adv, bh + adv, idesc, 1);
+              tc_mma_bf16(d, ah + adv, bl + adv, idesc, 1);
+            }
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;  // TMEM lane quarter == tile row block
+    float* buf = epi_buf + q * 32 * 33;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const int m0 = (tile / num_n) * GEMM_BM;
+      const int n0 = (tile % num_n) * BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row0 = m0 + q * 32;
+      const int rows = min(32, args.M - row0);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld_32x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = v[i];
+        __syncwarp();
+        const int col = n0 + c + lane;
+        const float b = args.bias[col];
+#pragma unroll 4
+        for (int r = 0; r < rows; ++r) {
+          const size_t row = (size_t)(row0 + r);
+          float x = buf[r * 33 + lane] + b;
+          if (EPI == EPI_F32) {
+            args.out_f32[row * args.ldo + col] = x;
+          } else if (EPI == EPI_F32_RES) {
+            x += args.residual[row * args.ldr + col];
+            args.out_f32[row * args.ldo + col] = x;
+          } else {
+            x = (EPI == EPI_GELU_SPLIT) ? gelu_tanh(x) : tanhf(x);
+            __nv_bfloat16 hi, lo;
+            split_bf16(x, hi, lo);
+            args.out_hi[row * args.ldh + col] = hi;
+            if (args.out_lo) args.out_lo[row * args.ldh + col] = lo;
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+}  // namespace mfg

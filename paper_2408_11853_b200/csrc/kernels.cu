@@ -1,0 +1,363 @@
+// Non-GEMM kernels of the scoring path (sm_100a). Activations are token-packed
+// ("varlen"): all sequences of all roles of a chunk are concatenated into one
+// [T, d] stream; cu_seqlens[s]..cu_seqlens[s+1] are the rows of sequence s.
+// Padded columns (d..ld) of every activation buffer are zero and stay zero.
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace mfg {
+
+// ------------------------------------------------------------------ embedding
+// x_p = E_tok[id_p] + E_pos[p]   (`pkg/src/metricforge/encoder.py:166-168`)
+__global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ pos,
+                             int T, int d, const float* __restrict__ tok,
+                             const float* __restrict__ pe, float* __restrict__ x32, int ld,
+                             __nv_bfloat16* __restrict__ xh, __nv_bfloat16* __restrict__ xl) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const float* a = tok + (size_t)ids[t] * d;
+  const float* b = pe + (size_t)pos[t] * d;
+  const size_t o = (size_t)t * ld;
+  for (int c = lane; c < d; c += 32) {
+    const float v = a[c] + b[c];
+    x32[o + c] = v;
+    if (xh) {
+      __nv_bfloat16 h, l;
+      split_bf16(v, h, l);
+      xh[o + c] = h;
+      if (xl) xl[o + c] = l;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ layer norm
+// out = (y - mean) / sqrt(var_pop + 1e-5) * g + b, one warp per row
+// (`encoder.py:52-57, 128-130`). Writes any of: fp32 copy, bf16 hi, bf16 lo.
+template <int VPT>
+__global__ void layernorm_kernel(const float* __restrict__ y, int T, int d, int ld,
+                                 const float* __restrict__ g, const float* __restrict__ bta,
+                                 float* __restrict__ out32, __nv_bfloat16* __restrict__ oh,
+                                 __nv_bfloat16* __restrict__ ol) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const float* row = y + (size_t)t * ld;
+  float v[VPT];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = i * 32 + lane;
+    v[i] = (c < d) ? row[c] : 0.f;
+    s += v[i];
+  }
+  const float mean = warp_sum(s) / (float)d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = i * 32 + lane;
+    const float z = (c < d) ? v[i] - mean : 0.f;
+    q += z * z;
+  }
+  const float var = warp_sum(q) / (float)d;
+  const float rstd = 1.0f / sqrtf(var + 1e-5f);
+  const size_t o = (size_t)t * ld;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = i * 32 + lane;
+    if (c < d) {
+      const float r = (v[i] - mean) * rstd * g[c] + bta[c];
+      if (out32) out32[o + c] = r;
+      if (oh) {
+        __nv_bfloat16 h, l;
+        split_bf16(r, h, l);
+        oh[o + c] = h;
+        if (ol) ol[o + c] = l;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ attention
+// Exact (non-approximate) fp32 masked-softmax attention per (sequence, head),
+// flash-style over 64-key blocks (`encoder.py:132-147`, `masked_softmax` 60-66).
+// PAD keys never exist in the packed layout; keys past the sequence end inside
+// the last block get -inf and therefore exactly zero weight.
+// CTA = 128 threads = 16 row groups x 8 column groups; a thread owns 4 query
+// rows x 8 keys of S and 4 rows x DHC output columns (column = cg + 8*i).
+constexpr int ATT_BQ = 64, ATT_BK = 64, ATT_THREADS = 128;
+
+template <int DHC>
+__global__ void __launch_bounds__(ATT_THREADS)
+    attention_kernel(const float* __restrict__ qkv, int ldq, int d, int dh, float scale,
+                     const int32_t* __restrict__ cu, const int2* __restrict__ work,
+                     __nv_bfloat16* __restrict__ ch, __nv_bfloat16* __restrict__ cl, int ldc) {
+  constexpr int DHMAX = DHC * 8;
+  constexpr int STR = DHMAX + 1;
+  extern __shared__ float sm[];
+  float* Qs = sm;                   // [BQ][STR]
+  float* Ks = Qs + ATT_BQ * STR;    // [BK][STR]
+  float* Vs = Ks + ATT_BK * STR;    // [BK][STR]
+  float* Ps = Vs + ATT_BK * STR;    // [BQ][BK+1]
+
+  const int2 w = work[blockIdx.x];
+  const int seq = w.x, q0 = w.y;
+  const int h = blockIdx.y;
+  const int start = cu[seq];
+  const int L = cu[seq + 1] - start;
+  const int nq = min(ATT_BQ, L - q0);
+  const int tid = threadIdx.x;
+  const int rg = tid >> 3, cg = tid & 7;
+
+  const float* qbase = qkv + (size_t)start * ldq + h * dh;
+  for (int i = tid; i < ATT_BQ * DHMAX; i += ATT_THREADS) {
+    const int r = i / DHMAX, c = i % DHMAX;
+    Qs[r * STR + c] = (r < nq && c < dh) ? qbase[(size_t)(q0 + r) * ldq + c] : 0.f;
+  }
+
+  float m[4], l[4], o[4][DHC];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    m[a] = -INFINITY;
+    l[a] = 0.f;
+#pragma unroll
+    for (int i = 0; i < DHC; ++i) o[a][i] = 0.f;
+  }
+
+  for (int k0 = 0; k0 < L; k0 += ATT_BK) {
+    const int nk = min(ATT_BK, L - k0);
+    __syncthreads();
+    const float* kb = qkv + (size_t)(start + k0) * ldq + d + h * dh;
+    const float* vb = kb + d;
+    for (int i = tid; i < ATT_BK * DHMAX; i += ATT_THREADS) {
+      const int r = i / DHMAX, c = i % DHMAX;
+      const bool ok = r < nk && c < dh;
+      Ks[r * STR + c] = ok ? kb[(size_t)r * ldq + c] : 0.f;
+      Vs[r * STR + c] = ok ? vb[(size_t)r * ldq + c] : 0.f;
+    }
+    __syncthreads();
+
+    float s[4][8];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s[a][j] = 0.f;
+    for (int c = 0; c < dh; ++c) {
+      float qv[4], kv[8];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) qv[a] = Qs[(rg * 4 + a) * STR + c];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) kv[j] = Ks[(cg + 8 * j) * STR + c];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s[a][j] = fmaf(qv[a], kv[j], s[a][j]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      float mx = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        s[a][j] = (cg + 8 * j < nk) ? s[a][j] * scale : -INFINITY;
+        mx = fmaxf(mx, s[a][j]);
+      }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+      const float mn = fmaxf(m[a], mx);
+      const float corr = expf(m[a] - mn);  // exp(-inf) = 0 on the first block
+      float sum = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float p = expf(s[a][j] - mn);
+        sum += p;
+        Ps[(rg * 4 + a) * (ATT_BK + 1) + cg + 8 * j] = p;
+      }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+      l[a] = l[a] * corr + sum;
+      m[a] = mn;
+#pragma unroll
+      for (int i = 0; i < DHC; ++i) o[a][i] *= corr;
+    }
+    __syncthreads();
+    for (int j = 0; j < nk; ++j) {
+      float pv[4], vv[DHC];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) pv[a] = Ps[(rg * 4 + a) * (ATT_BK + 1) + j];
+#pragma unroll
+      for (int i = 0; i < DHC; ++i) vv[i] = Vs[j * STR + cg + 8 * i];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int i = 0; i < DHC; ++i) o[a][i] = fmaf(pv[a], vv[i], o[a][i]);
+    }
+  }
+
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int r = rg * 4 + a;
+    if (r >= nq) continue;
+    const float inv = 1.0f / l[a];
+    const size_t ob = (size_t)(start + q0 + r) * ldc + h * dh;
+#pragma unroll
+    for (int i = 0; i < DHC; ++i) {
+      const int c = cg + 8 * i;
+      if (c < dh) {
+        __nv_bfloat16 hh, ll;
+        split_bf16(o[a][i] * inv, hh, ll);
+        ch[ob + c] = hh;
+        if (cl) cl[ob + c] = ll;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ features
+// BOS pooling (`encoder.py:181-185`) + per-kind feature vector (`:198-212`),
+// written as the bf16 hi/lo A-operand of the first head GEMM.
+// kind: 0 = comet-qe [t,s,t*s,|t-s|], 1 = comet [t,r,t*s,t*r,|t-s|,|t-r|], 2 = bleurt [j]
+__global__ void features_kernel(const float* __restrict__ x, int ld, int d, int kind,
+                                const int32_t* __restrict__ cu, int n,
+                                __nv_bfloat16* __restrict__ fh, __nv_bfloat16* __restrict__ fl,
+                                int ldf) {
+  const int r = blockIdx.x;
+  const size_t ro = (size_t)r * ldf;
+  const float* p0 = x + (size_t)cu[r] * ld;
+  const float* p1 = kind != 2 ? x + (size_t)cu[n + r] * ld : nullptr;
+  const float* p2 = kind == 1 ? x + (size_t)cu[2 * n + r] * ld : nullptr;
+  auto put = [&](int c, float v) {
+    __nv_bfloat16 h, l;
+    split_bf16(v, h, l);
+    fh[ro + c] = h;
+    if (fl) fl[ro + c] = l;
+  };
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    if (kind == 0) {
+      const float s = p0[c], t = p1[c];
+      put(c, t);
+      put(d + c, s);
+      put(2 * d + c, t * s);
+      put(3 * d + c, fabsf(t - s));
+    } else if (kind == 1) {
+      const float s = p0[c], t = p1[c], rr = p2[c];
+      put(c, t);
+      put(d + c, rr);
+      put(2 * d + c, t * s);
+      put(3 * d + c, t * rr);
+      put(4 * d + c, fabsf(t - s));
+      put(5 * d + c, fabsf(t - rr));
+    } else {
+      put(c, p0[c]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ weight prep
+// W[K][N] fp32 (row-vector x matrix, `pkg/README.md:137-140`) -> Wᵀ as bf16 hi
+// (and lo) [Npad][Kpad], placed at row offset `row0` of the destination, zero
+// padding untouched (destination is zero-initialised).
+__global__ void transpose_split_kernel(const float* __restrict__ w, int K, int N,
+                                       __nv_bfloat16* __restrict__ hi,
+                                       __nv_bfloat16* __restrict__ lo, int ldk, int row0) {
+  __shared__ float tile[32][33];
+  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int k = k0 + i, n = n0 + threadIdx.x;
+    tile[i][threadIdx.x] = (k < K && n < N) ? w[(size_t)k * N + n] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int n = n0 + i, k = k0 + threadIdx.x;
+    if (n < N && k < K) {
+      __nv_bfloat16 h, l;
+      split_bf16(tile[threadIdx.x][i], h, l);
+      const size_t o = (size_t)(row0 + n) * ldk + k;
+      hi[o] = h;
+      if (lo) lo[o] = l;
+    }
+  }
+}
+
+// scores[i] = out[i * ld]  (column 0 of the final head stage, `encoder.py:196`)
+__global__ void gather_col0_kernel(const float* __restrict__ out, int ld, int n,
+                                   float* __restrict__ scores) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) scores[i] = out[(size_t)i * ld];
+}
+
+// ------------------------------------------------------------------ launchers
+cudaError_t launch_embed(const int32_t* ids, const int32_t* pos, int T, int d, const float* tok,
+                         const float* pe, float* x32, int ld, __nv_bfloat16* xh,
+                         __nv_bfloat16* xl, cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  embed_kernel<<<(T + 7) / 8, 256, 0, st>>>(ids, pos, T, d, tok, pe, x32, ld, xh, xl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_layernorm(const float* y, int T, int d, int ld, const float* g, const float* b,
+                             float* out32, __nv_bfloat16* oh, __nv_bfloat16* ol,
+                             cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  const int vpt = (d + 31) / 32;
+  dim3 grid((T + 7) / 8), block(256);
+#define LN_CASE(V)                                                                   \
+  if (vpt <= V) {                                                                    \
+    layernorm_kernel<V><<<grid, block, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol);   \
+    return cudaGetLastError();                                                       \
+  }
+  LN_CASE(1) LN_CASE(2) LN_CASE(4) LN_CASE(8) LN_CASE(16) LN_CASE(24) LN_CASE(32)
+  LN_CASE(36) LN_CASE(40) LN_CASE(48) LN_CASE(64) LN_CASE(80) LN_CASE(96) LN_CASE(128)
+#undef LN_CASE
+  return cudaErrorInvalidValue;
+}
+
+template <int DHC>
+static cudaError_t att_launch(const float* qkv, int ldq, int d, int dh, float scale,
+                              const int32_t* cu, const int2* work, int n_work, int heads,
+                              __nv_bfloat16* ch, __nv_bfloat16* cl, int ldc, cudaStream_t st) {
+  constexpr int STR = DHC * 8 + 1;
+  const size_t smem = sizeof(float) * (3 * 64 * STR + 64 * 65);
+  cudaFuncSetAttribute(attention_kernel<DHC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  attention_kernel<DHC><<<dim3(n_work, heads), ATT_THREADS, smem, st>>>(qkv, ldq, d, dh, scale,
+                                                                         cu, work, ch, cl, ldc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attention(const float* qkv, int ldq, int d, int heads, const int32_t* cu,
+                             const int2* work, int n_work, __nv_bfloat16* ch,
+                             __nv_bfloat16* cl, int ldc, cudaStream_t st) {
+  if (n_work <= 0) return cudaSuccess;
+  const int dh = d / heads;
+  const float scale = 1.0f / sqrtf((float)d / (float)heads);
+  const int dhc = (dh + 7) / 8;
+#define ATT_CASE(V) \
+  if (dhc <= V) return att_launch<V>(qkv, ldq, d, dh, scale, cu, work, n_work, heads, ch, cl, ldc, st);
+  ATT_CASE(1) ATT_CASE(2) ATT_CASE(4) ATT_CASE(8) ATT_CASE(10) ATT_CASE(12) ATT_CASE(16)
+#undef ATT_CASE
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_features(const float* x, int ld, int d, int kind, const int32_t* cu, int n,
+                            __nv_bfloat16* fh, __nv_bfloat16* fl, int ldf, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  features_kernel<<<n, 256, 0, st>>>(x, ld, d, kind, cu, n, fh, fl, ldf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transpose_split(const float* w, int K, int N, __nv_bfloat16* hi,
+                                   __nv_bfloat16* lo, int ldk, int row0, cudaStream_t st) {
+  dim3 grid((N + 31) / 32, (K + 31) / 32), block(32, 8);
+  transpose_split_kernel<<<grid, block, 0, st>>>(w, K, N, hi, lo, ldk, row0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_col0(const float* out, int ld, int n, float* scores, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  gather_col0_kernel<<<(n + 255) / 256, 256, 0, st>>>(out, ld, n, scores);
+  return cudaGetLastError();
+}
+
+}  // namespace mfg

@@ -1,0 +1,783 @@
+// libmfgpu: scoring context and C-ABI (include/mfgpu.h).
+//
+// Replaces `ScoringModel` (`pkg/src/metricforge/encoder.py:94-226`): weights are
+// uploaded once, matrices transposed to K-major and split into bf16 hi/lo pairs
+// (fp32-parity) or rounded to bf16 (bf16 mode); a batch of records is scored as
+// one token-packed stream per device chunk.
+#include <cerrno>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mfgpu.h"
+#include "../../include/mfgpu_test.h"
+#include "container.hpp"
+#include "gemm_tc.cuh"
+#include "kernels.h"
+
+using namespace mfg;
+
+namespace {
+
+thread_local int g_code = 0;
+thread_local std::string g_msg;
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t _e = (x);                                                                  \
+    if (_e != cudaSuccess)                                                                 \
+      throw Fail{MFG_ERR_RUNTIME, std::string("CUDA error: ") + cudaGetErrorString(_e) +   \
+                                      " at " #x};                                          \
+  } while (0)
+
+inline int pad64(int64_t x) { return (int)((x + 63) / 64 * 64); }
+inline int64_t pad128(int64_t x) { return (x + 127) / 128 * 128; }
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+};
+
+// A GEMM weight: Wᵀ as bf16 hi (+lo) [Npad][Kpad], bias [Npad], tensor maps.
+struct Weight {
+  __nv_bfloat16 *hi = nullptr, *lo = nullptr;
+  float* bias = nullptr;
+  int N = 0, K = 0, Npad = 0, Kpad = 0, bn = 64;
+  CUtensorMap mh{}, ml{};
+};
+
+// A GEMM A-operand activation buffer [rows][ld] bf16 hi (+lo).
+struct Act {
+  __nv_bfloat16 *hi = nullptr, *lo = nullptr;
+  int64_t rows = 0;
+  int ld = 0;
+  CUtensorMap mh{}, ml{};
+};
+
+struct Layer {
+  Weight qkv, o, w1, w2;
+  float *g1 = nullptr, *b1 = nullptr, *g2 = nullptr, *b2 = nullptr;
+};
+
+enum Cls { C_QKV = 0, C_O, C_FFN1, C_FFN2, C_ATT, C_LN, C_EMB, C_HEAD };
+
+}  // namespace
+
+struct mfg_ctx {
+  int device = 0, precision = MFG_PREC_FP32, num_sms = 148;
+  bool split = true, pre_norm = false, profile = false;
+  Manifest man;
+  int kind = 0, n_roles = 0;
+  int d = 0, dp = 0, f = 0, fp = 0, H = 0, F = 0, Fp = 0, qkv_ld = 0;
+  cudaStream_t st = nullptr;
+  std::vector<void*> allocs;
+  int64_t device_bytes = 0;
+
+  float *tok = nullptr, *pos = nullptr;
+  std::vector<Layer> layers;
+  std::vector<Weight> head;
+
+  int64_t cap_tokens = 0;
+  int cap_records = 0;
+  float *x32 = nullptr, *y32 = nullptr, *qkv = nullptr;
+  Act xa, ca, ha, fa;
+  std::vector<Act> ga;  // head hidden-stage outputs
+  float* hout = nullptr;
+  float* dscores = nullptr;
+  int32_t *d_ids = nullptr, *d_pos = nullptr, *d_cu = nullptr;
+  int2* d_work = nullptr;
+  int32_t *h_ids = nullptr, *h_pos = nullptr, *h_cu = nullptr;
+  int2* h_work = nullptr;
+  float* h_scores = nullptr;
+  int64_t work_cap = 0;
+
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<cudaEvent_t> pev;  // profile event pool
+  struct Rec {
+    int cls;
+    int e0, e1;
+  };
+  std::vector<Rec> recs;
+  int pev_used = 0;
+  mfg_stats stats{};
+
+  int err_code = 0;
+  std::string err_msg;
+
+  template <class T>
+  T* dalloc(size_t count) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    allocs.push_back(p);
+    device_bytes += (int64_t)(count * sizeof(T));
+    CK(cudaMemsetAsync(p, 0, count * sizeof(T), st));
+    return (T*)p;
+  }
+
+  // ---------------------------------------------------------------- profiling
+  int ev_begin() {
+    if (!profile) return -1;
+    if (pev_used + 2 > (int)pev.size()) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        pev.push_back(e);
+      }
+    }
+    int i = pev_used;
+    pev_used += 2;
+    CK(cudaEventRecord(pev[i], st));
+    return i;
+  }
+  void ev_end(int i, int cls, double flops, double bytes) {
+    stats.kernel_launches += 1;
+    stats.class_launches[cls] += 1;
+    stats.class_flops[cls] += flops;
+    stats.class_bytes[cls] += bytes;
+    if (i < 0) return;
+    CK(cudaEventRecord(pev[i + 1], st));
+    recs.push_back({cls, i, i + 1});
+  }
+  void collect_profile() {
+    for (auto& r : recs) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, pev[r.e0], pev[r.e1]));
+      stats.class_ms[r.cls] += ms;
+    }
+    recs.clear();
+    pev_used = 0;
+  }
+
+  // ---------------------------------------------------------------- setup
+  void make_act(Act& a, int64_t rows, int cols_pad) {
+    char err[256];
+    a.rows = pad128(rows);
+    a.ld = cols_pad;
+    a.hi = dalloc<__nv_bfloat16>((size_t)a.rows * a.ld);
+    if (!make_tmap_bf16(&a.mh, a.hi, a.rows, a.ld, a.ld, GEMM_BM, err, sizeof err))
+      throw Fail{MFG_ERR_RUNTIME, err};
+    if (split) {
+      a.lo = dalloc<__nv_bfloat16>((size_t)a.rows * a.ld);
+      if (!make_tmap_bf16(&a.ml, a.lo, a.rows, a.ld, a.ld, GEMM_BM, err, sizeof err))
+        throw Fail{MFG_ERR_RUNTIME, err};
+    }
+  }
+
+  // Upload one or more fp32 [K][N_i] matrices side by side along N as a single Wᵀ.
+  void make_weight(Weight& w, const std::vector<const TensorView*>& mats,
+                   const std::vector<const TensorView*>& biases, float* staging_dev,
+                   std::vector<float>& host_tmp) {
+    char err[256];
+    w.K = (int)mats[0]->shape[0];
+    w.N = 0;
+    for (auto* m : mats) w.N += (int)m->shape[1];
+    w.Kpad = pad64(w.K);
+    w.Npad = pad64(w.N);
+    w.bn = gemm_pick_bn(w.Npad);
+    w.hi = dalloc<__nv_bfloat16>((size_t)w.Npad * w.Kpad);
+    if (split) w.lo = dalloc<__nv_bfloat16>((size_t)w.Npad * w.Kpad);
+    int row0 = 0;
+    for (auto* m : mats) {
+      const float* src = host_f32(*m, host_tmp);
+      CK(cudaMemcpyAsync(staging_dev, src, m->numel() * 4, cudaMemcpyHostToDevice, st));
+      CK(launch_transpose_split(staging_dev, (int)m->shape[0], (int)m->shape[1], w.hi, w.lo,
+                                w.Kpad, row0, st));
+      CK(cudaStreamSynchronize(st));
+      row0 += (int)m->shape[1];
+    }
+    w.bias = dalloc<float>(w.Npad);
+    int off = 0;
+    for (auto* b : biases) {
+      const float* src = host_f32(*b, host_tmp);
+      CK(cudaMemcpy(w.bias + off, src, b->numel() * 4, cudaMemcpyHostToDevice));
+      off += (int)b->numel();
+    }
+    if (!make_tmap_bf16(&w.mh, w.hi, w.Npad, w.Kpad, w.Kpad, w.bn, err, sizeof err))
+      throw Fail{MFG_ERR_RUNTIME, err};
+    if (split && !make_tmap_bf16(&w.ml, w.lo, w.Npad, w.Kpad, w.Kpad, w.bn, err, sizeof err))
+      throw Fail{MFG_ERR_RUNTIME, err};
+  }
+
+  static const float* host_f32(const TensorView& t, std::vector<float>& tmp) {
+    if (t.dtype == "f32") return reinterpret_cast<const float*>(t.data);
+    // binary16 -> fp32 (exact), as `tensor.astype(float32)` in the reference
+    tmp.resize(t.numel());
+    const uint16_t* h = reinterpret_cast<const uint16_t*>(t.data);
+    for (int64_t i = 0; i < t.numel(); ++i) {
+      uint32_t s = (h[i] & 0x8000u) << 16, e = (h[i] >> 10) & 0x1F, m = h[i] & 0x3FF, bits;
+      if (e == 0) {
+        if (m == 0) bits = s;
+        else {
+          e = 127 - 15 + 1;
+          while (!(m & 0x400)) { m <<= 1; --e; }
+          bits = s | (e << 23) | ((m & 0x3FF) << 13);
+        }
+      } else if (e == 31) bits = s | 0x7F800000u | (m << 13);
+      else bits = s | ((e + 127 - 15) << 23) | (m << 13);
+      memcpy(&tmp[i], &bits, 4);
+    }
+    return tmp.data();
+  }
+
+  float* upload_vec(const TensorView& t, size_t pad_to = 0) {
+    std::vector<float> tmp;
+    const float* src = host_f32(t, tmp);
+    float* p = dalloc<float>(std::max<size_t>(pad_to, (size_t)t.numel()));
+    CK(cudaMemcpy(p, src, t.numel() * 4, cudaMemcpyHostToDevice));
+    return p;
+  }
+
+  void build(const mfg_config& cfg) {
+    Container c(cfg.container_path);
+    man = c.manifest();
+    if (man.like == "comet-qe") { kind = 0; n_roles = 2; }
+    else if (man.like == "comet") { kind = 1; n_roles = 3; }
+    else if (man.like == "bleurt") { kind = 2; n_roles = 1; }
+    else throw Fail{MFG_ERR_CONTAINER, "unknown metric kind '" + man.like + "'"};
+    if (man.d_model <= 0 || man.n_heads <= 0 || man.d_model % man.n_heads != 0)
+      throw Fail{MFG_ERR_CONTAINER, "d_model not divisible by n_heads"};
+    pre_norm = man.norm_style == "pre";
+    // shape contract (encoder.py:107-115)
+    for (auto& kv : required_shapes(man)) {
+      const TensorView* t = c.find(kv.first);
+      if (!t) throw Fail{MFG_ERR_CONTAINER, c.path() + ": missing tensor '" + kv.first + "'"};
+      if (t->shape != kv.second)
+        throw Fail{MFG_ERR_CONTAINER, c.path() + ": tensor '" + kv.first + "' has shape " +
+                                          shape_repr(t->shape) + ", manifest implies " +
+                                          shape_repr(kv.second)};
+    }
+    d = (int)man.d_model;
+    dp = pad64(d);
+    f = (int)man.d_ffn;
+    fp = pad64(f);
+    H = (int)man.n_heads;
+    F = feature_multiplier(man.like) * d;
+    Fp = pad64(F);
+    if (d / H > 128) throw Fail{MFG_ERR_CONTAINER, "head dimension > 128 is not supported"};
+
+    // staging buffer for the largest matrix upload
+    int64_t big = 0;
+    for (auto& kv : required_shapes(man))
+      if (kv.second.size() == 2 && kv.first.rfind("emb.", 0) != 0) {
+        int64_t n = kv.second[0] * kv.second[1];
+        big = std::max(big, n);
+      }
+    float* staging = nullptr;
+    CK(cudaMalloc(&staging, std::max<int64_t>(big, 1) * 4));
+    std::vector<float> tmp;
+    try {
+      tok = upload_vec(*c.find("emb.tok"));
+      pos = upload_vec(*c.find("emb.pos"));
+      layers.resize(man.n_layers);
+      for (int i = 0; i < man.n_layers; ++i) {
+        std::string p = "layer." + std::to_string(i);
+        Layer& L = layers[i];
+        auto T = [&](const std::string& n) { return c.find(p + n); };
+        make_weight(L.qkv, {T(".att.q.w"), T(".att.k.w"), T(".att.v.w")},
+                    {T(".att.q.b"), T(".att.k.b"), T(".att.v.b")}, staging, tmp);
+        make_weight(L.o, {T(".att.o.w")}, {T(".att.o.b")}, staging, tmp);
+        make_weight(L.w1, {T(".ffn.w1")}, {T(".ffn.b1")}, staging, tmp);
+        make_weight(L.w2, {T(".ffn.w2")}, {T(".ffn.b2")}, staging, tmp);
+        L.g1 = upload_vec(*T(".norm1.g"));
+        L.b1 = upload_vec(*T(".norm1.b"));
+        L.g2 = upload_vec(*T(".norm2.g"));
+        L.b2 = upload_vec(*T(".norm2.b"));
+      }
+      const size_t stages = man.head_hidden.size() + 1;
+      head.resize(stages);
+      for (size_t j = 0; j < stages; ++j) {
+        std::string p = "head." + std::to_string(j);
+        make_weight(head[j], {c.find(p + ".w")}, {c.find(p + ".b")}, staging, tmp);
+      }
+    } catch (...) {
+      cudaFree(staging);
+      throw;
+    }
+    CK(cudaStreamSynchronize(st));
+    CK(cudaFree(staging));
+    qkv_ld = layers.empty() ? pad64(3 * d) : layers[0].qkv.Npad;
+
+    // workspaces
+    cap_tokens = pad128(cfg.max_tokens > 0 ? cfg.max_tokens : 262144);
+    cap_records = cfg.max_records > 0 ? cfg.max_records : 4096;
+    x32 = dalloc<float>((size_t)cap_tokens * dp);
+    y32 = dalloc<float>((size_t)cap_tokens * dp);
+    qkv = dalloc<float>((size_t)cap_tokens * qkv_ld);
+    make_act(xa, cap_tokens, dp);
+    make_act(ca, cap_tokens, dp);
+    make_act(ha, cap_tokens, fp);
+    make_act(fa, cap_records, Fp);
+    ga.resize(head.size() - 1);
+    for (size_t j = 0; j + 1 < head.size(); ++j) make_act(ga[j], cap_records, head[j].Npad);
+    hout = dalloc<float>((size_t)pad128(cap_records) * head.back().Npad);
+    dscores = dalloc<float>(cap_records);
+    d_ids = dalloc<int32_t>(cap_tokens);
+    d_pos = dalloc<int32_t>(cap_tokens);
+    d_cu = dalloc<int32_t>((size_t)cap_records * n_roles + 1);
+    work_cap = cap_tokens / 1 + (int64_t)cap_records * n_roles;
+    d_work = dalloc<int2>(work_cap);
+    CK(cudaMallocHost(&h_ids, cap_tokens * 4));
+    CK(cudaMallocHost(&h_pos, cap_tokens * 4));
+    CK(cudaMallocHost(&h_cu, ((size_t)cap_records * n_roles + 1) * 4));
+    CK(cudaMallocHost(&h_work, work_cap * sizeof(int2)));
+    CK(cudaMallocHost(&h_scores, cap_records * 4));
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    CK(cudaStreamSynchronize(st));
+  }
+
+  // ---------------------------------------------------------------- forward
+  void gemm(const Act& a, const Weight& w, int M, int epi, int cls, const float* res, int ldr,
+            float* out32, int ldo, Act* outa) {
+    GemmArgs g{};
+    g.M = M;
+    g.N = w.Npad;
+    g.K = w.Kpad;
+    g.bias = w.bias;
+    g.residual = res;
+    g.ldr = ldr;
+    g.out_f32 = out32;
+    g.ldo = ldo;
+    if (outa) {
+      g.out_hi = outa->hi;
+      g.out_lo = outa->lo;
+      g.ldh = outa->ld;
+    }
+    int e = ev_begin();
+    CK(launch_gemm(&a.mh, split ? &a.ml : &a.mh, &w.mh, split ? &w.ml : &w.mh, w.bn, split, epi,
+                   g, num_sms, st));
+    const double flops = 2.0 * M * (double)w.N * w.K;
+    double bytes = (double)M * w.K * (split ? 4 : 2) + (double)w.N * w.K * (split ? 4 : 2);
+    bytes += (double)M * w.N * (epi == EPI_F32 ? 4 : epi == EPI_F32_RES ? 8 : (split ? 4 : 2));
+    ev_end(e, cls, flops, bytes);
+  }
+
+  void layernorm(const float* y, int T, const float* g, const float* b, float* out32, Act* a) {
+    int e = ev_begin();
+    CK(launch_layernorm(y, T, d, dp, g, b, out32, a ? a->hi : nullptr, a ? a->lo : nullptr, st));
+    ev_end(e, C_LN, 0, (double)T * d * (4 + (out32 ? 4 : 0) + (a ? (split ? 4 : 2) : 0)));
+  }
+
+  // One device chunk: m records, T tokens, role-major packing in h_* staging.
+  void forward_chunk(int m, int64_t T, int64_t n_work, double sum_l2, float* scores_out) {
+    const int nseq = m * n_roles;
+    CK(cudaMemcpyAsync(d_ids, h_ids, T * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_pos, h_pos, T * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_cu, h_cu, (nseq + 1) * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_work, h_work, n_work * sizeof(int2), cudaMemcpyHostToDevice, st));
+    const int Ti = (int)T;
+    {
+      int e = ev_begin();
+      CK(launch_embed(d_ids, d_pos, Ti, d, tok, pos, x32, dp, pre_norm ? nullptr : xa.hi,
+                      pre_norm ? nullptr : xa.lo, st));
+      ev_end(e, C_EMB, 0, (double)T * d * (8 + 4 + (pre_norm ? 0 : (split ? 4 : 2))));
+    }
+    for (auto& L : layers) {
+      if (pre_norm) layernorm(x32, Ti, L.g1, L.b1, nullptr, &xa);
+      gemm(xa, L.qkv, Ti, EPI_F32, C_QKV, nullptr, 0, qkv, qkv_ld, nullptr);
+      {
+        int e = ev_begin();
+        CK(launch_attention(qkv, qkv_ld, d, H, d_cu, d_work, (int)n_work, ca.hi, ca.lo, ca.ld,
+                            st));
+        ev_end(e, C_ATT, 4.0 * sum_l2 * d, (double)T * d * (12 + (split ? 4 : 2)));
+      }
+      gemm(ca, L.o, Ti, EPI_F32_RES, C_O, x32, dp, y32, dp, nullptr);
+      if (!pre_norm) {
+        layernorm(y32, Ti, L.g1, L.b1, x32, &xa);
+        gemm(xa, L.w1, Ti, EPI_GELU_SPLIT, C_FFN1, nullptr, 0, nullptr, 0, &ha);
+        gemm(ha, L.w2, Ti, EPI_F32_RES, C_FFN2, x32, dp, y32, dp, nullptr);
+        layernorm(y32, Ti, L.g2, L.b2, x32, &xa);
+      } else {
+        layernorm(y32, Ti, L.g2, L.b2, nullptr, &xa);
+        gemm(xa, L.w1, Ti, EPI_GELU_SPLIT, C_FFN1, nullptr, 0, nullptr, 0, &ha);
+        gemm(ha, L.w2, Ti, EPI_F32_RES, C_FFN2, y32, dp, x32, dp, nullptr);
+      }
+    }
+    {
+      int e = ev_begin();
+      CK(launch_features(x32, dp, d, kind, d_cu, m, fa.hi, fa.lo, fa.ld, st));
+      ev_end(e, C_HEAD, 0, (double)m * (n_roles * d * 4 + F * (split ? 4 : 2)));
+    }
+    const Act* in = &fa;
+    for (size_t j = 0; j < head.size(); ++j) {
+      const bool last = j + 1 == head.size();
+      if (last) {
+        gemm(*in, head[j], m, EPI_F32, C_HEAD, nullptr, 0, hout, head[j].Npad, nullptr);
+      } else {
+        gemm(*in, head[j], m, EPI_TANH_SPLIT, C_HEAD, nullptr, 0, nullptr, 0, &ga[j]);
+        in = &ga[j];
+      }
+    }
+    {
+      int e = ev_begin();
+      CK(launch_gather_col0(hout, head.back().Npad, m, dscores, st));
+      ev_end(e, C_HEAD, 0, (double)m * 8);
+    }
+    CK(cudaMemcpyAsync(h_scores, dscores, m * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    memcpy(scores_out, h_scores, m * 4);
+  }
+
+  void score(int32_t n, int32_t n_roles_in, const int32_t* ids, const int64_t* cu, float* out) {
+    if (n < 0) throw Fail{MFG_ERR_USAGE, "n_records must be >= 0"};
+    if (n_roles_in != n_roles)
+      throw Fail{MFG_ERR_USAGE, "model kind '" + man.like + "' scores " + std::to_string(n_roles) +
+                                    " sequences per record, got " + std::to_string(n_roles_in)};
+    if (n == 0) return;
+    const int64_t nseq = (int64_t)n * n_roles;
+    if (cu[0] != 0) throw Fail{MFG_ERR_USAGE, "cu_seqlens[0] must be 0"};
+    for (int64_t s = 0; s < nseq; ++s) {
+      const int64_t L = cu[s + 1] - cu[s];
+      if (L > man.max_position)
+        throw Fail{MFG_ERR_USAGE, "sequence length " + std::to_string(L) +
+                                      " exceeds limit " + std::to_string(man.max_position)};
+      if (L <= 0) throw Fail{MFG_ERR_USAGE, "cannot pool a row with no tokens"};
+    }
+    const int64_t total = cu[nseq];
+    for (int64_t t = 0; t < total; ++t)
+      if (ids[t] < 0 || ids[t] >= man.vocab_size)
+        throw Fail{MFG_ERR_USAGE,
+                   "token id out of range for vocab_size " + std::to_string(man.vocab_size)};
+
+    CK(cudaEventRecord(ev0, st));
+    int r0 = 0;
+    while (r0 < n) {
+      // greedy chunk by records within token / record / work capacity
+      int r1 = r0;
+      int64_t T = 0, W = 0;
+      while (r1 < n && r1 - r0 < cap_records) {
+        int64_t t = 0, w = 0;
+        for (int k = 0; k < n_roles; ++k) {
+          const int64_t L = cu[(int64_t)k * n + r1 + 1] - cu[(int64_t)k * n + r1];
+          t += L;
+          w += (L + 63) / 64;
+        }
+        if (T + t > cap_tokens || W + w > work_cap) break;
+        T += t;
+        W += w;
+        ++r1;
+      }
+      if (r1 == r0) throw Fail{MFG_ERR_USAGE, "record exceeds device chunk capacity"};
+      const int m = r1 - r0;
+      // pack role-major
+      int64_t at = 0, nw = 0;
+      double sum_l2 = 0;
+      h_cu[0] = 0;
+      for (int k = 0; k < n_roles; ++k)
+        for (int r = r0; r < r1; ++r) {
+          const int64_t s = (int64_t)k * n + r;
+          const int64_t L = cu[s + 1] - cu[s];
+          memcpy(h_ids + at, ids + cu[s], L * 4);
+          for (int64_t p = 0; p < L; ++p) h_pos[at + p] = (int32_t)p;
+          const int ls = k * m + (r - r0);
+          for (int64_t q = 0; q < L; q += 64) h_work[nw++] = make_int2(ls, (int)q);
+          at += L;
+          h_cu[ls + 1] = (int32_t)at;
+          sum_l2 += (double)L * L;
+        }
+      forward_chunk(m, T, nw, sum_l2 * man.n_layers, out + r0);
+      stats.tokens += T;
+      stats.chunks += 1;
+      r0 = r1;
+    }
+    CK(cudaEventRecord(ev1, st));
+    CK(cudaEventSynchronize(ev1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    stats.device_ms += ms;
+    stats.calls += 1;
+    stats.records += n;
+    if (profile) collect_profile();
+  }
+
+  ~mfg_ctx() {
+    if (st) cudaStreamSynchronize(st);
+    for (void* p : allocs) cudaFree(p);
+    if (h_ids) cudaFreeHost(h_ids);
+    if (h_pos) cudaFreeHost(h_pos);
+    if (h_cu) cudaFreeHost(h_cu);
+    if (h_work) cudaFreeHost(h_work);
+    if (h_scores) cudaFreeHost(h_scores);
+    for (auto e : pev) cudaEventDestroy(e);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+// ======================================================================= C-ABI
+static int set_global(int code, const std::string& msg) {
+  g_code = code;
+  g_msg = msg;
+  return code;
+}
+
+extern "C" int mfg_create(const mfg_config* cfg, mfg_ctx** out) {
+  if (!cfg || !out || !cfg->container_path) return set_global(MFG_ERR_USAGE, "null argument");
+  *out = nullptr;
+  mfg_ctx* c = new mfg_ctx();
+  try {
+    if (cfg->precision != MFG_PREC_FP32 && cfg->precision != MFG_PREC_BF16)
+      throw Fail{MFG_ERR_USAGE, "unknown precision " + std::to_string(cfg->precision)};
+    c->device = cfg->device;
+    c->precision = cfg->precision;
+    c->split = cfg->precision == MFG_PREC_FP32;
+    c->profile = cfg->profile != 0;
+    CK(cudaSetDevice(c->device));
+    int major = 0, minor = 0;
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c->device));
+    CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, c->device));
+    if (major != 10 || minor != 0)
+      throw Fail{MFG_ERR_RUNTIME, "libmfgpu is built for sm_100a (B200); device is sm_" +
+                                      std::to_string(major) + std::to_string(minor)};
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    c->build(*cfg);
+  } catch (const Fail& f) {
+    delete c;
+    return set_global(f.code, f.msg);
+  } catch (const ContainerError& e) {
+    delete c;
+    return set_global(MFG_ERR_CONTAINER, e.what());
+  } catch (const std::exception& e) {
+    delete c;
+    return set_global(MFG_ERR_RUNTIME, e.what());
+  }
+  *out = c;
+  return set_global(MFG_OK, "");
+}
+
+extern "C" int mfg_score_batch(mfg_ctx* c, int32_t n, int32_t n_roles, const int32_t* ids,
+                               const int64_t* cu, float* scores) {
+  if (!c) return set_global(MFG_ERR_USAGE, "null context");
+  try {
+    CK(cudaSetDevice(c->device));
+    c->score(n, n_roles, ids, cu, scores);
+  } catch (const Fail& f) {
+    c->err_code = f.code;
+    c->err_msg = f.msg;
+    return f.code;
+  } catch (const std::exception& e) {
+    c->err_code = MFG_ERR_RUNTIME;
+    c->err_msg = e.what();
+    return MFG_ERR_RUNTIME;
+  }
+  c->err_code = 0;
+  c->err_msg.clear();
+  return MFG_OK;
+}
+
+extern "C" int mfg_last_error(const mfg_ctx* c, int32_t* code, char* buf, size_t cap) {
+  const int cd = c ? c->err_code : g_code;
+  const std::string& m = c ? c->err_msg : g_msg;
+  if (code) *code = cd;
+  if (buf && cap) {
+    size_t k = std::min(cap - 1, m.size());
+    memcpy(buf, m.data(), k);
+    buf[k] = 0;
+  }
+  return MFG_OK;
+}
+
+extern "C" void mfg_destroy(mfg_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  delete c;
+}
+
+extern "C" int mfg_get_model_info(const mfg_ctx* c, mfg_model_info* o) {
+  if (!c || !o) return MFG_ERR_USAGE;
+  o->kind = c->kind;
+  o->vocab_size = (int32_t)c->man.vocab_size;
+  o->d_model = c->d;
+  o->n_heads = c->H;
+  o->n_layers = (int32_t)c->man.n_layers;
+  o->d_ffn = c->f;
+  o->max_position = (int32_t)c->man.max_position;
+  o->pre_norm = c->pre_norm;
+  o->n_roles = c->n_roles;
+  o->n_head_stages = (int32_t)c->head.size();
+  o->precision = c->precision;
+  o->num_sms = c->num_sms;
+  o->device_bytes = c->device_bytes;
+  return MFG_OK;
+}
+
+extern "C" int mfg_get_stats(const mfg_ctx* c, mfg_stats* o) {
+  if (!c || !o) return MFG_ERR_USAGE;
+  *o = c->stats;
+  return MFG_OK;
+}
+
+extern "C" int mfg_reset_stats(mfg_ctx* c) {
+  if (!c) return MFG_ERR_USAGE;
+  c->stats = mfg_stats{};
+  return MFG_OK;
+}
+
+// ================================================================= test entry points
+namespace {
+struct Scratch {
+  std::vector<void*> ps;
+  template <class T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    ps.push_back(p);
+    CK(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)));
+    return (T*)p;
+  }
+  ~Scratch() {
+    for (void* p : ps) cudaFree(p);
+  }
+};
+
+__global__ void split_rows_kernel(const float* src, int rows, int cols, __nv_bfloat16* hi,
+                                  __nv_bfloat16* lo, int ld) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)rows * cols) return;
+  const int r = (int)(i / cols), c = (int)(i % cols);
+  __nv_bfloat16 h, l;
+  split_bf16(src[i], h, l);
+  hi[(int64_t)r * ld + c] = h;
+  if (lo) lo[(int64_t)r * ld + c] = l;
+}
+__global__ void join_rows_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int ld,
+                                 int rows, int cols, float* dst) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)rows * cols) return;
+  const int r = (int)(i / cols), c = (int)(i % cols);
+  float v = __bfloat162float(hi[(int64_t)r * ld + c]);
+  if (lo) v += __bfloat162float(lo[(int64_t)r * ld + c]);
+  dst[i] = v;
+}
+
+template <class F>
+int guarded(F&& fn) {
+  try {
+    fn();
+  } catch (const Fail& f) {
+    return set_global(f.code, f.msg);
+  } catch (const std::exception& e) {
+    return set_global(MFG_ERR_RUNTIME, e.what());
+  }
+  return set_global(MFG_OK, "");
+}
+}  // namespace
+
+extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, int32_t K,
+                         const float* A, const float* W, const float* bias,
+                         const float* residual, float* out) {
+  return guarded([&] {
+    const bool split = precision == MFG_PREC_FP32;
+    int dev = 0, sms = 148;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    Scratch s;
+    char err[256];
+    const int Kp = pad64(K), Np = pad64(N);
+    const int64_t Mp = pad128(M);
+    const int bn = gemm_pick_bn(Np);
+    float* dA = s.alloc<float>((size_t)M * K);
+    float* dW = s.alloc<float>((size_t)K * N);
+    CK(cudaMemcpy(dA, A, (size_t)M * K * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dW, W, (size_t)K * N * 4, cudaMemcpyHostToDevice));
+    auto* ah = s.alloc<__nv_bfloat16>(Mp * Kp);
+    auto* al = split ? s.alloc<__nv_bfloat16>(Mp * Kp) : nullptr;
+    auto* wh = s.alloc<__nv_bfloat16>((size_t)Np * Kp);
+    auto* wl = split ? s.alloc<__nv_bfloat16>((size_t)Np * Kp) : nullptr;
+    const int64_t tot = (int64_t)M * K;
+    split_rows_kernel<<<(unsigned)((tot + 255) / 256), 256>>>(dA, M, K, ah, al, Kp);
+    CK(cudaGetLastError());
+    CK(launch_transpose_split(dW, K, N, wh, wl, Kp, 0, 0));
+    float* db = s.alloc<float>(Np);
+    if (bias) CK(cudaMemcpy(db, bias, N * 4, cudaMemcpyHostToDevice));
+    float* dr = s.alloc<float>((size_t)M * Np);
+    if (residual)
+      CK(cudaMemcpy2D(dr, Np * 4, residual, N * 4, N * 4, M, cudaMemcpyHostToDevice));
+    float* d32 = s.alloc<float>((size_t)M * Np);
+    auto* oh = s.alloc<__nv_bfloat16>((size_t)M * Np);
+    auto* ol = split ? s.alloc<__nv_bfloat16>((size_t)M * Np) : nullptr;
+    CUtensorMap mah, mal, mwh, mwl;
+    if (!make_tmap_bf16(&mah, ah, Mp, Kp, Kp, GEMM_BM, err, sizeof err) ||
+        !make_tmap_bf16(&mwh, wh, Np, Kp, Kp, bn, err, sizeof err))
+      throw Fail{MFG_ERR_RUNTIME, err};
+    if (split && (!make_tmap_bf16(&mal, al, Mp, Kp, Kp, GEMM_BM, err, sizeof err) ||
+                  !make_tmap_bf16(&mwl, wl, Np, Kp, Kp, bn, err, sizeof err)))
+      throw Fail{MFG_ERR_RUNTIME, err};
+    GemmArgs g{};
+    g.M = M;
+    g.N = Np;
+    g.K = Kp;
+    g.bias = db;
+    g.residual = dr;
+    g.ldr = Np;
+    g.out_f32 = d32;
+    g.ldo = Np;
+    g.out_hi = oh;
+    g.out_lo = ol;
+    g.ldh = Np;
+    CK(launch_gemm(&mah, split ? &mal : &mah, &mwh, split ? &mwl : &mwh, bn, split, epi, g, sms, 0));
+    CK(cudaDeviceSynchronize());
+    if (epi == EPI_F32 || epi == EPI_F32_RES) {
+      CK(cudaMemcpy2D(out, N * 4, d32, Np * 4, N * 4, M, cudaMemcpyDeviceToHost));
+    } else {
+      float* tmpd = s.alloc<float>((size_t)M * N);
+      join_rows_kernel<<<(unsigned)(((int64_t)M * N + 255) / 256), 256>>>(oh, ol, Np, M, N, tmpd);
+      CK(cudaGetLastError());
+      CK(cudaMemcpy(out, tmpd, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+extern "C" int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* cu, int32_t d,
+                              int32_t n_heads, const float* qkv, float* ctx_out) {
+  return guarded([&] {
+    const bool split = precision == MFG_PREC_FP32;
+    Scratch s;
+    const int T = cu[n_seq];
+    const int ldq = pad64(3 * d), ldc = pad64(d);
+    float* dq = s.alloc<float>((size_t)T * ldq);
+    CK(cudaMemcpy2D(dq, ldq * 4, qkv, 3 * d * 4, 3 * d * 4, T, cudaMemcpyHostToDevice));
+    int32_t* dcu = s.alloc<int32_t>(n_seq + 1);
+    CK(cudaMemcpy(dcu, cu, (n_seq + 1) * 4, cudaMemcpyHostToDevice));
+    std::vector<int2> work;
+    for (int i = 0; i < n_seq; ++i)
+      for (int q = 0; q < cu[i + 1] - cu[i]; q += 64) work.push_back(make_int2(i, q));
+    int2* dw = s.alloc<int2>(work.size());
+    CK(cudaMemcpy(dw, work.data(), work.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    auto* ch = s.alloc<__nv_bfloat16>((size_t)T * ldc);
+    auto* cl = split ? s.alloc<__nv_bfloat16>((size_t)T * ldc) : nullptr;
+    CK(launch_attention(dq, ldq, d, n_heads, dcu, dw, (int)work.size(), ch, cl, ldc, 0));
+    float* o = s.alloc<float>((size_t)T * d);
+    join_rows_kernel<<<(unsigned)(((int64_t)T * d + 255) / 256), 256>>>(ch, cl, ldc, T, d, o);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(ctx_out, o, (size_t)T * d * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+extern "C" int mfgt_layernorm(int32_t T, int32_t d, const float* y, const float* g,
+                              const float* b, float* out) {
+  return guarded([&] {
+    Scratch s;
+    float* dy = s.alloc<float>((size_t)T * d);
+    float* dg = s.alloc<float>(d);
+    float* db = s.alloc<float>(d);
+    float* dout = s.alloc<float>((size_t)T * d);
+    CK(cudaMemcpy(dy, y, (size_t)T * d * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dg, g, d * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(db, b, d * 4, cudaMemcpyHostToDevice));
+    CK(launch_layernorm(dy, T, d, d, dg, db, dout, nullptr, nullptr, 0));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out, dout, (size_t)T * d * 4, cudaMemcpyDeviceToHost));
+  });
+}

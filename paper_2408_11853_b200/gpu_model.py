@@ -1,0 +1,153 @@
+"""`GpuScoringModel`: the device replacement of the reference `ScoringModel`.
+
+Same constructor shape `(container, compute_mode)` and the same
+`score_records(encoded_records) -> np.float32[n]` contract as
+`pkg/src/metricforge/encoder.py:94-226`, implemented by libmfgpu
+(include/mfgpu.h) on one B200. `score_packed` is the zero-copy fast path used
+by `Evaluator`: role-major token ids + cu_seqlens straight from libmfhost.
+
+Precisions (`EvaluatorConfig.precision`):
+  "fp32"  bf16x3 split operands on tcgen05, fp32 accumulate — the parity path
+          (|Δ| ≤ 1e-3 per segment against the fp32 reference)
+  "bf16"  single bf16 MMA per k-step — reported separately with its error stats
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+import threading
+
+import numpy as np
+
+from . import native
+from .errors import ContainerError, DeviceError
+from .kinds import N_SEQUENCES, Kind
+
+PRECISIONS = {"fp32": 0, "bf16": 1}
+
+
+class ComputeMode(enum.Enum):
+    FP32 = "fp32"
+    FP16 = "fp16"
+
+    @classmethod
+    def parse(cls, value):
+        if isinstance(value, cls):
+            return value
+        try:
+            return cls(value)
+        except ValueError:
+            raise ValueError(f"unknown compute mode {value!r}") from None
+
+
+def default_precision(compute_mode) -> str:
+    """fp32 keeps the parity path; the reference's fp16 flag (binary16
+    storage) selects the reduced-precision bf16 device path."""
+    return "fp32" if ComputeMode.parse(compute_mode) is ComputeMode.FP32 else "bf16"
+
+
+def _device_ordinal(device) -> int:
+    if device is None:
+        return int(os.environ.get("LOCAL_RANK", "0")) if os.environ.get("MFG_DEVICE_FROM_RANK") else 0
+    if isinstance(device, int):
+        return device
+    s = str(device)
+    if s.startswith("cuda"):
+        return int(s.split(":", 1)[1]) if ":" in s else 0
+    return int(s)
+
+
+class GpuScoringModel:
+    def __init__(self, container, compute_mode=ComputeMode.FP32, device=None, precision=None,
+                 max_tokens=0, max_records=0, profile=False):
+        path = container if isinstance(container, (str, os.PathLike)) else container.path
+        self.manifest = None if isinstance(container, (str, os.PathLike)) else container.manifest
+        self.mode = ComputeMode.parse(compute_mode)
+        self.precision = precision or default_precision(self.mode)
+        if self.precision not in PRECISIONS:
+            raise ValueError(f"unknown precision {self.precision!r} (known: fp32, bf16)")
+        self._lib = native.gpu()
+        cfg = native.MfgConfig(os.fsencode(str(path)), _device_ordinal(device),
+                               PRECISIONS[self.precision], int(max_tokens), int(max_records),
+                               int(bool(profile)))
+        handle = C.c_void_p()
+        rc = self._lib.mfg_create(C.byref(cfg), C.byref(handle))
+        if rc != 0:
+            code, msg = native.last_error(None)
+            raise (ContainerError if rc == 3 else ValueError if rc == 2 else DeviceError)(msg)
+        self._h = handle
+        self._lock = threading.Lock()
+        info = native.MfgModelInfo()
+        self._lib.mfg_get_model_info(self._h, C.byref(info))
+        self.info = info
+        self.kind = Kind.parse(("comet-qe", "comet", "bleurt")[info.kind])
+        self.n_roles = int(info.n_roles)
+        self.max_position = int(info.max_position)
+        self.vocab_size = int(info.vocab_size)
+
+    # ------------------------------------------------------------------ core
+    def score_packed(self, ids, cu_seqlens, n_records) -> np.ndarray:
+        """ids int32 role-major, cu_seqlens int64[n_roles*n+1] -> float32[n]."""
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        cu = np.ascontiguousarray(cu_seqlens, dtype=np.int64)
+        out = np.empty(n_records, dtype=np.float32)
+        if n_records == 0:
+            return out
+        with self._lock:
+            if self._h is None:
+                raise DeviceError("scoring model is closed")
+            rc = self._lib.mfg_score_batch(self._h, int(n_records), self.n_roles,
+                                           native.ptr(ids, C.c_int32), native.ptr(cu, C.c_int64),
+                                           native.ptr(out, C.c_float))
+            if rc != 0:
+                _, msg = native.last_error(self._h)
+                raise (ValueError if rc == 2 else ContainerError if rc == 3 else DeviceError)(msg)
+        return out
+
+    def score_records(self, encoded_records) -> np.ndarray:
+        """`encoded_records`: per record, the TokenSequence list of encode_fields
+        for this model's kind (role order). Returns float32 scores in order."""
+        n = len(encoded_records)
+        seqs = [encoded_records[i][k].ids for k in range(self.n_roles) for i in range(n)]
+        lens = np.fromiter((len(s) for s in seqs), dtype=np.int64, count=len(seqs))
+        if n and lens.max() > self.max_position:  # pad_batch's check (batching.py:83-86)
+            raise ValueError(f"sequence length {int(lens.max())} exceeds limit {self.max_position}")
+        cu = np.zeros(len(seqs) + 1, dtype=np.int64)
+        np.cumsum(lens, out=cu[1:])
+        ids = np.fromiter((t for s in seqs for t in s), dtype=np.int64, count=int(cu[-1]))
+        if ids.size and (ids.min() < 0 or ids.max() >= self.vocab_size):
+            raise ValueError(f"token id out of range for vocab_size {self.vocab_size}")
+        return self.score_packed(ids.astype(np.int32), cu, n)
+
+    # ------------------------------------------------------------------ stats
+    def stats(self) -> dict:
+        s = native.MfgStats()
+        self._lib.mfg_get_stats(self._h, C.byref(s))
+        out = {k: getattr(s, k) for k in ("device_ms", "calls", "records", "tokens", "chunks",
+                                           "kernel_launches")}
+        out["classes"] = {
+            name: {"ms": s.class_ms[i], "launches": s.class_launches[i],
+                   "flops": s.class_flops[i], "bytes": s.class_bytes[i]}
+            for i, name in enumerate(native.CLASS_NAMES)}
+        return out
+
+    def reset_stats(self):
+        self._lib.mfg_reset_stats(self._h)
+
+    def close(self):
+        with self._lock:
+            if self._h is not None:
+                self._lib.mfg_destroy(self._h)
+                self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def n_sequences(kind) -> int:
+    return N_SEQUENCES[Kind.parse(kind)]

@@ -1,0 +1,127 @@
+"""Kernel-level parity of libmfgpu against plain fp32 numpy references,
+through the C-ABI test entry points (include/mfgpu_test.h)."""
+
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2408_11853_b200 import native
+    return native.gpu()
+
+
+def _p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _gemm(lib, prec, epi, A, W, bias, res=None):
+    M, K = A.shape
+    N = W.shape[1]
+    out = np.zeros((M, N), np.float32)
+    rc = lib.mfgt_gemm(prec, epi, M, N, K, _p(A), _p(W), _p(bias),
+                       _p(res) if res is not None else None, _p(out))
+    if rc != 0:
+        from paper_2408_11853_b200 import native
+        pytest.fail(native.last_error(None)[1])
+    return out
+
+
+def _ref(epi, A, W, bias, res):
+    y = A.astype(np.float64) @ W.astype(np.float64) + bias
+    if epi == 1:
+        y = y + res
+    if epi == 2:
+        c = math.sqrt(2 / math.pi)
+        y = 0.5 * y * (1 + np.tanh(c * (y + 0.044715 * y ** 3)))
+    if epi == 3:
+        y = np.tanh(y)
+    return y
+
+
+SHAPES = [(1, 16, 16), (37, 48, 16), (130, 64, 64), (200, 256, 128), (256, 512, 256),
+          (300, 1024, 1024), (129, 1152, 192), (64, 3456, 1152), (5, 1, 40)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+def test_gemm_split_parity(lib, M, N, K, epi):
+    rng = np.random.default_rng(M * 1000 + N + K + epi)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    W = (rng.standard_normal((K, N)) / math.sqrt(K)).astype(np.float32)
+    b = (0.1 * rng.standard_normal(N)).astype(np.float32)
+    r = rng.standard_normal((M, N)).astype(np.float32)
+    got = _gemm(lib, 0, epi, A, W, b, r)
+    want = _ref(epi, A, W, b, r)
+    # bf16x3 keeps ~16 mantissa bits per operand: far below 1e-3 of the output scale
+    tol = 2e-4 * (1 + np.abs(want))
+    assert np.all(np.abs(got - want) <= tol), float(np.abs(got - want).max())
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES[:6])
+def test_gemm_bf16_mode(lib, M, N, K):
+    rng = np.random.default_rng(7 + M)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    W = (rng.standard_normal((K, N)) / math.sqrt(K)).astype(np.float32)
+    b = np.zeros(N, np.float32)
+    got = _gemm(lib, 1, 0, A, W, b)
+    want = _ref(0, A, W, b, None)
+    assert np.abs(got - want).max() <= 0.03 * (1 + np.abs(want).max())
+    # bf16 inputs exactly reproduce a bf16-rounded fp32 product
+    import torch
+    Ab = torch.from_numpy(A).bfloat16().double().numpy()
+    Wb = torch.from_numpy(W).bfloat16().double().numpy()
+    assert np.allclose(got, Ab @ Wb, atol=1e-4, rtol=1e-4)
+
+
+def _attn_ref(qkv, cu, d, H):
+    out = np.zeros((qkv.shape[0], d), np.float64)
+    dh = d // H
+    for s in range(len(cu) - 1):
+        a, b = cu[s], cu[s + 1]
+        for h in range(H):
+            q = qkv[a:b, h * dh:(h + 1) * dh].astype(np.float64)
+            k = qkv[a:b, d + h * dh:d + (h + 1) * dh].astype(np.float64)
+            v = qkv[a:b, 2 * d + h * dh:2 * d + (h + 1) * dh].astype(np.float64)
+            s_ = q @ k.T / math.sqrt(dh)
+            p = np.exp(s_ - s_.max(axis=1, keepdims=True))
+            p /= p.sum(axis=1, keepdims=True)
+            out[a:b, h * dh:(h + 1) * dh] = p @ v
+    return out
+
+
+@pytest.mark.parametrize("d,H,lens", [(16, 2, [3, 1, 7]), (64, 4, [65, 2, 130]),
+                                      (1024, 16, [128, 3, 64, 100]), (256, 4, [512]),
+                                      (2560, 32, [70, 9]), (1152, 18, [127])])
+def test_attention_parity(lib, d, H, lens):
+    rng = np.random.default_rng(d + len(lens))
+    cu = np.zeros(len(lens) + 1, np.int32)
+    cu[1:] = np.cumsum(lens)
+    T = int(cu[-1])
+    qkv = (2 * rng.standard_normal((T, 3 * d))).astype(np.float32)
+    out = np.zeros((T, d), np.float32)
+    rc = lib.mfgt_attention(0, len(lens), cu.ctypes.data_as(C.POINTER(C.c_int32)), d, H,
+                            _p(qkv), _p(out))
+    assert rc == 0
+    want = _attn_ref(qkv, cu, d, H)
+    assert np.abs(out - want).max() <= 1e-4 * (1 + np.abs(want).max())
+
+
+@pytest.mark.parametrize("T,d", [(1, 16), (33, 256), (100, 1024), (7, 1152), (5, 2560)])
+def test_layernorm_parity(lib, T, d):
+    rng = np.random.default_rng(T + d)
+    y = (3 * rng.standard_normal((T, d)) + 1).astype(np.float32)
+    g = (1 + 0.1 * rng.standard_normal(d)).astype(np.float32)
+    b = (0.1 * rng.standard_normal(d)).astype(np.float32)
+    out = np.zeros_like(y)
+    assert lib.mfgt_layernorm(T, d, _p(y), _p(g), _p(b), _p(out)) == 0
+    y64 = y.astype(np.float64)
+    mu = y64.mean(1, keepdims=True)
+    var = ((y64 - mu) ** 2).mean(1, keepdims=True)
+    want = (y64 - mu) / np.sqrt(var + 1e-5) * g + b
+    assert np.abs(out - want).max() <= 2e-5 * (1 + np.abs(want).max())
