@@ -34,8 +34,10 @@ extern "C" {
 #define MFG_ERR_CONTAINER 3
 
 /* Arithmetic of the encoder/head GEMMs. */
-#define MFG_PREC_FP32 0 /* fp32-parity: bf16x3 split operands on tcgen05 (|d| <= 1e-3 vs fp32 ref) */
-#define MFG_PREC_BF16 1 /* single bf16 MMA per k-step, fp32 accumulate (reported separately) */
+#define MFG_PREC_FP32 0   /* fp32-parity: fp16 hi/lo split operands, 3 tcgen05 MMAs per k-step
+                             (~22 significant bits; |d| <= 1e-3 vs the fp32 reference) */
+#define MFG_PREC_BF16 1   /* one bf16 MMA per k-step, fp32 accumulate (reported separately) */
+#define MFG_PREC_BF16X3 2 /* bf16 hi/lo split, 3 MMAs: fp32 range, ~16 significant bits */
 
 typedef struct mfg_ctx mfg_ctx;
 

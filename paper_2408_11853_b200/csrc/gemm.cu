@@ -27,7 +27,7 @@ static PFN_encodeTiled get_encode_fn() {
   return fn;
 }
 
-bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
+bool make_tmap_u16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                     uint64_t ld_elems, uint32_t box_rows, char* err, size_t errcap) {
   PFN_encodeTiled enc = get_encode_fn();
   if (!enc) {
@@ -38,7 +38,7 @@ bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t c
   cuuint64_t strides[1] = {ld_elems * 2};
   cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(ptr), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -86,9 +86,10 @@ static cudaError_t run_epi(int epi, const CUtensorMap* ah, const CUtensorMap* al
 }
 
 cudaError_t launch_gemm(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* bh,
-                        const CUtensorMap* bl, int bn, bool split, int epi, const GemmArgs& a,
+                        const CUtensorMap* bl, int bn, int nsplit, int epi, const GemmArgs& a,
                         int num_sms, cudaStream_t st) {
   if (a.K % GEMM_BK != 0 || a.N % bn != 0) return cudaErrorInvalidValue;
+  const bool split = nsplit == 2;
   if (split) {
     if (bn == 256) return run_epi<256, true>(epi, ah, al, bh, bl, a, num_sms, st);
     if (bn == 128) return run_epi<128, true>(epi, ah, al, bh, bl, a, num_sms, st);

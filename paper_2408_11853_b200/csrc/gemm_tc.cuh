@@ -10,11 +10,11 @@
 //   EPI_GELU_SPLIT out = gelu_tanh(acc + bias) -> bf16 hi/lo (FFN1, `encoder.py:149-151`)
 //   EPI_TANH_SPLIT out = tanh(acc + bias)      -> bf16 hi/lo (head hidden stages, `:190-196`)
 //
-// SPLIT=true is the fp32-parity path ("bf16x3"): A = A_hi + A_lo and
-// B = B_hi + B_lo are bf16 pairs and every k-step issues
-//   D += A_hi·B_hi + A_lo·B_hi + A_hi·B_lo
-// into one fp32 TMEM accumulator (~16 mantissa bits per operand).
-// SPLIT=false is the plain bf16 path (one MMA per k-step).
+// SPLIT=true: A = A_hi + A_lo and B = B_hi + B_lo are pairs of 16-bit pieces
+// and every k-step issues  D += A_hi·B_hi + A_lo·B_hi + A_hi·B_lo  into one fp32
+// TMEM accumulator. With fp16 pieces (the fp32-parity path) each operand keeps
+// ~22 significant bits; with bf16 pieces ("bf16x3") ~16 bits over the fp32 range.
+// SPLIT=false is the plain one-MMA-per-k-step path.
 //
 // Roles (256 threads): warp0 lane0 = TMA producer, warp1 lane0 = MMA issuer,
 // warp2 = TMEM allocator, warps4-7 = epilogue (warp w owns TMEM lanes
@@ -35,9 +35,11 @@ struct GemmArgs {
   int ldr;
   float* out_f32;            // [M][ldo] (EPI_F32*)
   int ldo;
-  __nv_bfloat16* out_hi;     // [M][ldh] (split epilogues)
-  __nv_bfloat16* out_lo;     // may be null when the consumer GEMM is not split
+  uint16_t* out_hi;          // [M][ldh] (split epilogues), 16-bit pieces in `fmt`
+  uint16_t* out_lo;          // may be null when the consumer GEMM is not split
   int ldh;
+  int fmt;                   // FMT_F16 / FMT_BF16: operand format of A, B and out_hi/lo
+  int* ovf;                  // set to 1 when an fp16 output overflows
 };
 
 constexpr int GEMM_BM = 128;
@@ -145,7 +147,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, BN);
+      const uint32_t idesc = idesc_f16kind(GEMM_BM, BN, (uint32_t)args.fmt);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -213,10 +215,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             args.out_f32[row * args.ldo + col] = x;
           } else {
             x = (EPI == EPI_GELU_SPLIT) ? gelu_tanh(x) : tanhf(x);
-            __nv_bfloat16 hi, lo;
-            split_bf16(x, hi, lo);
-            args.out_hi[row * args.ldh + col] = hi;
-            if (args.out_lo) args.out_lo[row * args.ldh + col] = lo;
+            store_split(args.out_hi, args.out_lo, row * args.ldh + col, x, args.fmt, args.ovf);
           }
         }
         __syncwarp();

@@ -12,7 +12,8 @@ namespace mfg {
 __global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ pos,
                              int T, int d, const float* __restrict__ tok,
                              const float* __restrict__ pe, float* __restrict__ x32, int ld,
-                             __nv_bfloat16* __restrict__ xh, __nv_bfloat16* __restrict__ xl) {
+                             uint16_t* __restrict__ xh, uint16_t* __restrict__ xl, int fmt,
+                             int* ovf) {
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -22,12 +23,7 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __r
   for (int c = lane; c < d; c += 32) {
     const float v = a[c] + b[c];
     x32[o + c] = v;
-    if (xh) {
-      __nv_bfloat16 h, l;
-      split_bf16(v, h, l);
-      xh[o + c] = h;
-      if (xl) xl[o + c] = l;
-    }
+    if (xh) store_split(xh, xl, o + c, v, fmt, ovf);
   }
 }
 
@@ -37,8 +33,8 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __r
 template <int VPT>
 __global__ void layernorm_kernel(const float* __restrict__ y, int T, int d, int ld,
                                  const float* __restrict__ g, const float* __restrict__ bta,
-                                 float* __restrict__ out32, __nv_bfloat16* __restrict__ oh,
-                                 __nv_bfloat16* __restrict__ ol) {
+                                 float* __restrict__ out32, uint16_t* __restrict__ oh,
+                                 uint16_t* __restrict__ ol, int fmt, int* ovf) {
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -68,12 +64,7 @@ __global__ void layernorm_kernel(const float* __restrict__ y, int T, int d, int 
     if (c < d) {
       const float r = (v[i] - mean) * rstd * g[c] + bta[c];
       if (out32) out32[o + c] = r;
-      if (oh) {
-        __nv_bfloat16 h, l;
-        split_bf16(r, h, l);
-        oh[o + c] = h;
-        if (ol) ol[o + c] = l;
-      }
+      if (oh) store_split(oh, ol, o + c, r, fmt, ovf);
     }
   }
 }
@@ -91,7 +82,8 @@ template <int DHC>
 __global__ void __launch_bounds__(ATT_THREADS)
     attention_kernel(const float* __restrict__ qkv, int ldq, int d, int dh, float scale,
                      const int32_t* __restrict__ cu, const int2* __restrict__ work,
-                     __nv_bfloat16* __restrict__ ch, __nv_bfloat16* __restrict__ cl, int ldc) {
+                     uint16_t* __restrict__ ch, uint16_t* __restrict__ cl, int ldc, int fmt,
+                     int* ovf) {
   constexpr int DHMAX = DHC * 8;
   constexpr int STR = DHMAX + 1;
   extern __shared__ float sm[];
@@ -204,12 +196,7 @@ __global__ void __launch_bounds__(ATT_THREADS)
 #pragma unroll
     for (int i = 0; i < DHC; ++i) {
       const int c = cg + 8 * i;
-      if (c < dh) {
-        __nv_bfloat16 hh, ll;
-        split_bf16(o[a][i] * inv, hh, ll);
-        ch[ob + c] = hh;
-        if (cl) cl[ob + c] = ll;
-      }
+      if (c < dh) store_split(ch, cl, ob + c, o[a][i] * inv, fmt, ovf);
     }
   }
 }
@@ -220,19 +207,14 @@ __global__ void __launch_bounds__(ATT_THREADS)
 // kind: 0 = comet-qe [t,s,t*s,|t-s|], 1 = comet [t,r,t*s,t*r,|t-s|,|t-r|], 2 = bleurt [j]
 __global__ void features_kernel(const float* __restrict__ x, int ld, int d, int kind,
                                 const int32_t* __restrict__ cu, int n,
-                                __nv_bfloat16* __restrict__ fh, __nv_bfloat16* __restrict__ fl,
-                                int ldf) {
+                                uint16_t* __restrict__ fh, uint16_t* __restrict__ fl, int ldf,
+                                int fmt, int* ovf) {
   const int r = blockIdx.x;
   const size_t ro = (size_t)r * ldf;
   const float* p0 = x + (size_t)cu[r] * ld;
   const float* p1 = kind != 2 ? x + (size_t)cu[n + r] * ld : nullptr;
   const float* p2 = kind == 1 ? x + (size_t)cu[2 * n + r] * ld : nullptr;
-  auto put = [&](int c, float v) {
-    __nv_bfloat16 h, l;
-    split_bf16(v, h, l);
-    fh[ro + c] = h;
-    if (fl) fl[ro + c] = l;
-  };
+  auto put = [&](int c, float v) { store_split(fh, fl, ro + c, v, fmt, ovf); };
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
     if (kind == 0) {
       const float s = p0[c], t = p1[c];
@@ -259,8 +241,8 @@ __global__ void features_kernel(const float* __restrict__ x, int ld, int d, int 
 // (and lo) [Npad][Kpad], placed at row offset `row0` of the destination, zero
 // padding untouched (destination is zero-initialised).
 __global__ void transpose_split_kernel(const float* __restrict__ w, int K, int N,
-                                       __nv_bfloat16* __restrict__ hi,
-                                       __nv_bfloat16* __restrict__ lo, int ldk, int row0) {
+                                       uint16_t* __restrict__ hi, uint16_t* __restrict__ lo,
+                                       int ldk, int row0, int fmt, int* ovf) {
   __shared__ float tile[32][33];
   const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -270,13 +252,8 @@ __global__ void transpose_split_kernel(const float* __restrict__ w, int K, int N
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int n = n0 + i, k = k0 + threadIdx.x;
-    if (n < N && k < K) {
-      __nv_bfloat16 h, l;
-      split_bf16(tile[threadIdx.x][i], h, l);
-      const size_t o = (size_t)(row0 + n) * ldk + k;
-      hi[o] = h;
-      if (lo) lo[o] = l;
-    }
+    if (n < N && k < K)
+      store_split(hi, lo, (size_t)(row0 + n) * ldk + k, tile[threadIdx.x][i], fmt, ovf);
   }
 }
 
@@ -289,22 +266,22 @@ __global__ void gather_col0_kernel(const float* __restrict__ out, int ld, int n,
 
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_embed(const int32_t* ids, const int32_t* pos, int T, int d, const float* tok,
-                         const float* pe, float* x32, int ld, __nv_bfloat16* xh,
-                         __nv_bfloat16* xl, cudaStream_t st) {
+                         const float* pe, float* x32, int ld, uint16_t* xh, uint16_t* xl,
+                         int fmt, int* ovf, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  embed_kernel<<<(T + 7) / 8, 256, 0, st>>>(ids, pos, T, d, tok, pe, x32, ld, xh, xl);
+  embed_kernel<<<(T + 7) / 8, 256, 0, st>>>(ids, pos, T, d, tok, pe, x32, ld, xh, xl, fmt, ovf);
   return cudaGetLastError();
 }
 
 cudaError_t launch_layernorm(const float* y, int T, int d, int ld, const float* g, const float* b,
-                             float* out32, __nv_bfloat16* oh, __nv_bfloat16* ol,
+                             float* out32, uint16_t* oh, uint16_t* ol, int fmt, int* ovf,
                              cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
   const int vpt = (d + 31) / 32;
   dim3 grid((T + 7) / 8), block(256);
 #define LN_CASE(V)                                                                   \
   if (vpt <= V) {                                                                    \
-    layernorm_kernel<V><<<grid, block, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol);   \
+    layernorm_kernel<V><<<grid, block, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol, fmt, ovf);   \
     return cudaGetLastError();                                                       \
   }
   LN_CASE(1) LN_CASE(2) LN_CASE(4) LN_CASE(8) LN_CASE(16) LN_CASE(24) LN_CASE(32)
@@ -316,41 +293,44 @@ cudaError_t launch_layernorm(const float* y, int T, int d, int ld, const float* 
 template <int DHC>
 static cudaError_t att_launch(const float* qkv, int ldq, int d, int dh, float scale,
                               const int32_t* cu, const int2* work, int n_work, int heads,
-                              __nv_bfloat16* ch, __nv_bfloat16* cl, int ldc, cudaStream_t st) {
+                              uint16_t* ch, uint16_t* cl, int ldc, int fmt, int* ovf,
+                              cudaStream_t st) {
   constexpr int STR = DHC * 8 + 1;
   const size_t smem = sizeof(float) * (3 * 64 * STR + 64 * 65);
   cudaFuncSetAttribute(attention_kernel<DHC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   attention_kernel<DHC><<<dim3(n_work, heads), ATT_THREADS, smem, st>>>(qkv, ldq, d, dh, scale,
-                                                                         cu, work, ch, cl, ldc);
+                                                                         cu, work, ch, cl, ldc,
+                                                                         fmt, ovf);
   return cudaGetLastError();
 }
 
 cudaError_t launch_attention(const float* qkv, int ldq, int d, int heads, const int32_t* cu,
-                             const int2* work, int n_work, __nv_bfloat16* ch,
-                             __nv_bfloat16* cl, int ldc, cudaStream_t st) {
+                             const int2* work, int n_work, uint16_t* ch, uint16_t* cl,
+                             int ldc, int fmt, int* ovf, cudaStream_t st) {
   if (n_work <= 0) return cudaSuccess;
   const int dh = d / heads;
   const float scale = 1.0f / sqrtf((float)d / (float)heads);
   const int dhc = (dh + 7) / 8;
 #define ATT_CASE(V) \
-  if (dhc <= V) return att_launch<V>(qkv, ldq, d, dh, scale, cu, work, n_work, heads, ch, cl, ldc, st);
+  if (dhc <= V) return att_launch<V>(qkv, ldq, d, dh, scale, cu, work, n_work, heads, ch, cl, ldc, fmt, ovf, st);
   ATT_CASE(1) ATT_CASE(2) ATT_CASE(4) ATT_CASE(8) ATT_CASE(10) ATT_CASE(12) ATT_CASE(16)
 #undef ATT_CASE
   return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_features(const float* x, int ld, int d, int kind, const int32_t* cu, int n,
-                            __nv_bfloat16* fh, __nv_bfloat16* fl, int ldf, cudaStream_t st) {
+                            uint16_t* fh, uint16_t* fl, int ldf, int fmt, int* ovf,
+                            cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  features_kernel<<<n, 256, 0, st>>>(x, ld, d, kind, cu, n, fh, fl, ldf);
+  features_kernel<<<n, 256, 0, st>>>(x, ld, d, kind, cu, n, fh, fl, ldf, fmt, ovf);
   return cudaGetLastError();
 }
 
-cudaError_t launch_transpose_split(const float* w, int K, int N, __nv_bfloat16* hi,
-                                   __nv_bfloat16* lo, int ldk, int row0, cudaStream_t st) {
+cudaError_t launch_transpose_split(const float* w, int K, int N, uint16_t* hi, uint16_t* lo,
+                                   int ldk, int row0, int fmt, int* ovf, cudaStream_t st) {
   dim3 grid((N + 31) / 32, (K + 31) / 32), block(32, 8);
-  transpose_split_kernel<<<grid, block, 0, st>>>(w, K, N, hi, lo, ldk, row0);
+  transpose_split_kernel<<<grid, block, 0, st>>>(w, K, N, hi, lo, ldk, row0, fmt, ovf);
   return cudaGetLastError();
 }
 

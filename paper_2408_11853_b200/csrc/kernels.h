@@ -8,29 +8,31 @@
 namespace mfg {
 
 cudaError_t launch_embed(const int32_t* ids, const int32_t* pos, int T, int d, const float* tok,
-                         const float* pe, float* x32, int ld, __nv_bfloat16* xh,
-                         __nv_bfloat16* xl, cudaStream_t st);
+                         const float* pe, float* x32, int ld, uint16_t* xh, uint16_t* xl,
+                         int fmt, int* ovf, cudaStream_t st);
 cudaError_t launch_layernorm(const float* y, int T, int d, int ld, const float* g, const float* b,
-                             float* out32, __nv_bfloat16* oh, __nv_bfloat16* ol,
+                             float* out32, uint16_t* oh, uint16_t* ol, int fmt, int* ovf,
                              cudaStream_t st);
 cudaError_t launch_attention(const float* qkv, int ldq, int d, int heads, const int32_t* cu,
-                             const int2* work, int n_work, __nv_bfloat16* ch,
-                             __nv_bfloat16* cl, int ldc, cudaStream_t st);
+                             const int2* work, int n_work, uint16_t* ch, uint16_t* cl,
+                             int ldc, int fmt, int* ovf, cudaStream_t st);
 cudaError_t launch_features(const float* x, int ld, int d, int kind, const int32_t* cu, int n,
-                            __nv_bfloat16* fh, __nv_bfloat16* fl, int ldf, cudaStream_t st);
-cudaError_t launch_transpose_split(const float* w, int K, int N, __nv_bfloat16* hi,
-                                   __nv_bfloat16* lo, int ldk, int row0, cudaStream_t st);
+                            uint16_t* fh, uint16_t* fl, int ldf, int fmt, int* ovf,
+                            cudaStream_t st);
+cudaError_t launch_transpose_split(const float* w, int K, int N, uint16_t* hi, uint16_t* lo,
+                                   int ldk, int row0, int fmt, int* ovf, cudaStream_t st);
 cudaError_t launch_gather_col0(const float* out, int ld, int n, float* scores, cudaStream_t st);
 
 // ---- tcgen05 GEMM (gemm.cu)
 struct GemmArgs;
-// Encode a 2-D bf16 K-major tensor map (128B swizzle, box = 64 x box_rows).
-bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
+// Encode a 2-D 16-bit K-major tensor map (128B swizzle, box = 64 x box_rows).
+bool make_tmap_u16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                     uint64_t ld_elems, uint32_t box_rows, char* err, size_t errcap);
 // Largest supported N tile dividing n_pad (n_pad % 64 == 0).
 int gemm_pick_bn(int n_pad);
+// nsplit: 1 = one MMA per k-step (hi only), 2 = hi/lo pieces, 3 MMAs per k-step.
 cudaError_t launch_gemm(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* bh,
-                        const CUtensorMap* bl, int bn, bool split, int epi, const GemmArgs& a,
+                        const CUtensorMap* bl, int bn, int nsplit, int epi, const GemmArgs& a,
                         int num_sms, cudaStream_t st);
 
 }  // namespace mfg

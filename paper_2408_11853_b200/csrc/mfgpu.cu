@@ -48,7 +48,7 @@ struct DevBuf {
 
 // A GEMM weight: Wᵀ as bf16 hi (+lo) [Npad][Kpad], bias [Npad], tensor maps.
 struct Weight {
-  __nv_bfloat16 *hi = nullptr, *lo = nullptr;
+  uint16_t *hi = nullptr, *lo = nullptr;
   float* bias = nullptr;
   int N = 0, K = 0, Npad = 0, Kpad = 0, bn = 64;
   CUtensorMap mh{}, ml{};
@@ -56,7 +56,7 @@ struct Weight {
 
 // A GEMM A-operand activation buffer [rows][ld] bf16 hi (+lo).
 struct Act {
-  __nv_bfloat16 *hi = nullptr, *lo = nullptr;
+  uint16_t *hi = nullptr, *lo = nullptr;
   int64_t rows = 0;
   int ld = 0;
   CUtensorMap mh{}, ml{};
@@ -74,6 +74,9 @@ enum Cls { C_QKV = 0, C_O, C_FFN1, C_FFN2, C_ATT, C_LN, C_EMB, C_HEAD };
 struct mfg_ctx {
   int device = 0, precision = MFG_PREC_FP32, num_sms = 148;
   bool split = true, pre_norm = false, profile = false;
+  int fmt = FMT_F16;       // 16-bit operand format of every GEMM operand
+  int* d_ovf = nullptr;    // fp16 range overflow flag (set by any producer)
+  int* h_ovf = nullptr;
   Manifest man;
   int kind = 0, n_roles = 0;
   int d = 0, dp = 0, f = 0, fp = 0, H = 0, F = 0, Fp = 0, qkv_ld = 0;
@@ -161,12 +164,12 @@ struct mfg_ctx {
     char err[256];
     a.rows = pad128(rows);
     a.ld = cols_pad;
-    a.hi = dalloc<__nv_bfloat16>((size_t)a.rows * a.ld);
-    if (!make_tmap_bf16(&a.mh, a.hi, a.rows, a.ld, a.ld, GEMM_BM, err, sizeof err))
+    a.hi = dalloc<uint16_t>((size_t)a.rows * a.ld);
+    if (!make_tmap_u16(&a.mh, a.hi, a.rows, a.ld, a.ld, GEMM_BM, err, sizeof err))
       throw Fail{MFG_ERR_RUNTIME, err};
     if (split) {
-      a.lo = dalloc<__nv_bfloat16>((size_t)a.rows * a.ld);
-      if (!make_tmap_bf16(&a.ml, a.lo, a.rows, a.ld, a.ld, GEMM_BM, err, sizeof err))
+      a.lo = dalloc<uint16_t>((size_t)a.rows * a.ld);
+      if (!make_tmap_u16(&a.ml, a.lo, a.rows, a.ld, a.ld, GEMM_BM, err, sizeof err))
         throw Fail{MFG_ERR_RUNTIME, err};
     }
   }
@@ -182,14 +185,14 @@ struct mfg_ctx {
     w.Kpad = pad64(w.K);
     w.Npad = pad64(w.N);
     w.bn = gemm_pick_bn(w.Npad);
-    w.hi = dalloc<__nv_bfloat16>((size_t)w.Npad * w.Kpad);
-    if (split) w.lo = dalloc<__nv_bfloat16>((size_t)w.Npad * w.Kpad);
+    w.hi = dalloc<uint16_t>((size_t)w.Npad * w.Kpad);
+    if (split) w.lo = dalloc<uint16_t>((size_t)w.Npad * w.Kpad);
     int row0 = 0;
     for (auto* m : mats) {
       const float* src = host_f32(*m, host_tmp);
       CK(cudaMemcpyAsync(staging_dev, src, m->numel() * 4, cudaMemcpyHostToDevice, st));
       CK(launch_transpose_split(staging_dev, (int)m->shape[0], (int)m->shape[1], w.hi, w.lo,
-                                w.Kpad, row0, st));
+                                w.Kpad, row0, fmt, d_ovf, st));
       CK(cudaStreamSynchronize(st));
       row0 += (int)m->shape[1];
     }
@@ -200,9 +203,9 @@ struct mfg_ctx {
       CK(cudaMemcpy(w.bias + off, src, b->numel() * 4, cudaMemcpyHostToDevice));
       off += (int)b->numel();
     }
-    if (!make_tmap_bf16(&w.mh, w.hi, w.Npad, w.Kpad, w.Kpad, w.bn, err, sizeof err))
+    if (!make_tmap_u16(&w.mh, w.hi, w.Npad, w.Kpad, w.Kpad, w.bn, err, sizeof err))
       throw Fail{MFG_ERR_RUNTIME, err};
-    if (split && !make_tmap_bf16(&w.ml, w.lo, w.Npad, w.Kpad, w.Kpad, w.bn, err, sizeof err))
+    if (split && !make_tmap_u16(&w.ml, w.lo, w.Npad, w.Kpad, w.Kpad, w.bn, err, sizeof err))
       throw Fail{MFG_ERR_RUNTIME, err};
   }
 
@@ -273,6 +276,8 @@ struct mfg_ctx {
     float* staging = nullptr;
     CK(cudaMalloc(&staging, std::max<int64_t>(big, 1) * 4));
     std::vector<float> tmp;
+    d_ovf = dalloc<int>(1);
+    CK(cudaMallocHost(&h_ovf, sizeof(int)));
     try {
       tok = upload_vec(*c.find("emb.tok"));
       pos = upload_vec(*c.find("emb.pos"));
@@ -303,6 +308,10 @@ struct mfg_ctx {
     }
     CK(cudaStreamSynchronize(st));
     CK(cudaFree(staging));
+    CK(cudaMemcpy(h_ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost));
+    if (*h_ovf)
+      throw Fail{MFG_ERR_USAGE, "a weight exceeds the fp16 range of the fp32-parity path "
+                                "(|w| >= 65520); use precision bf16x3"};
     qkv_ld = layers.empty() ? pad64(3 * d) : layers[0].qkv.Npad;
 
     // workspaces
@@ -346,14 +355,16 @@ struct mfg_ctx {
     g.ldr = ldr;
     g.out_f32 = out32;
     g.ldo = ldo;
+    g.fmt = fmt;
+    g.ovf = d_ovf;
     if (outa) {
       g.out_hi = outa->hi;
       g.out_lo = outa->lo;
       g.ldh = outa->ld;
     }
     int e = ev_begin();
-    CK(launch_gemm(&a.mh, split ? &a.ml : &a.mh, &w.mh, split ? &w.ml : &w.mh, w.bn, split, epi,
-                   g, num_sms, st));
+    CK(launch_gemm(&a.mh, split ? &a.ml : &a.mh, &w.mh, split ? &w.ml : &w.mh, w.bn,
+                   split ? 2 : 1, epi, g, num_sms, st));
     const double flops = 2.0 * M * (double)w.N * w.K;
     double bytes = (double)M * w.K * (split ? 4 : 2) + (double)w.N * w.K * (split ? 4 : 2);
     bytes += (double)M * w.N * (epi == EPI_F32 ? 4 : epi == EPI_F32_RES ? 8 : (split ? 4 : 2));
@@ -362,7 +373,8 @@ struct mfg_ctx {
 
   void layernorm(const float* y, int T, const float* g, const float* b, float* out32, Act* a) {
     int e = ev_begin();
-    CK(launch_layernorm(y, T, d, dp, g, b, out32, a ? a->hi : nullptr, a ? a->lo : nullptr, st));
+    CK(launch_layernorm(y, T, d, dp, g, b, out32, a ? a->hi : nullptr, a ? a->lo : nullptr, fmt,
+                        d_ovf, st));
     ev_end(e, C_LN, 0, (double)T * d * (4 + (out32 ? 4 : 0) + (a ? (split ? 4 : 2) : 0)));
   }
 
@@ -373,11 +385,12 @@ struct mfg_ctx {
     CK(cudaMemcpyAsync(d_pos, h_pos, T * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d_cu, h_cu, (nseq + 1) * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d_work, h_work, n_work * sizeof(int2), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(d_ovf, 0, sizeof(int), st));
     const int Ti = (int)T;
     {
       int e = ev_begin();
       CK(launch_embed(d_ids, d_pos, Ti, d, tok, pos, x32, dp, pre_norm ? nullptr : xa.hi,
-                      pre_norm ? nullptr : xa.lo, st));
+                      pre_norm ? nullptr : xa.lo, fmt, d_ovf, st));
       ev_end(e, C_EMB, 0, (double)T * d * (8 + 4 + (pre_norm ? 0 : (split ? 4 : 2))));
     }
     for (auto& L : layers) {
@@ -386,7 +399,7 @@ struct mfg_ctx {
       {
         int e = ev_begin();
         CK(launch_attention(qkv, qkv_ld, d, H, d_cu, d_work, (int)n_work, ca.hi, ca.lo, ca.ld,
-                            st));
+                            fmt, d_ovf, st));
         ev_end(e, C_ATT, 4.0 * sum_l2 * d, (double)T * d * (12 + (split ? 4 : 2)));
       }
       gemm(ca, L.o, Ti, EPI_F32_RES, C_O, x32, dp, y32, dp, nullptr);
@@ -403,7 +416,7 @@ struct mfg_ctx {
     }
     {
       int e = ev_begin();
-      CK(launch_features(x32, dp, d, kind, d_cu, m, fa.hi, fa.lo, fa.ld, st));
+      CK(launch_features(x32, dp, d, kind, d_cu, m, fa.hi, fa.lo, fa.ld, fmt, d_ovf, st));
       ev_end(e, C_HEAD, 0, (double)m * (n_roles * d * 4 + F * (split ? 4 : 2)));
     }
     const Act* in = &fa;
@@ -422,7 +435,11 @@ struct mfg_ctx {
       ev_end(e, C_HEAD, 0, (double)m * 8);
     }
     CK(cudaMemcpyAsync(h_scores, dscores, m * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (*h_ovf)
+      throw Fail{MFG_ERR_RUNTIME, "an activation exceeded the fp16 range of the fp32-parity path "
+                                  "(|x| >= 65520); rerun with precision bf16x3"};
     memcpy(scores_out, h_scores, m * 4);
   }
 
@@ -506,6 +523,7 @@ struct mfg_ctx {
     if (h_cu) cudaFreeHost(h_cu);
     if (h_work) cudaFreeHost(h_work);
     if (h_scores) cudaFreeHost(h_scores);
+    if (h_ovf) cudaFreeHost(h_ovf);
     for (auto e : pev) cudaEventDestroy(e);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -525,11 +543,12 @@ extern "C" int mfg_create(const mfg_config* cfg, mfg_ctx** out) {
   *out = nullptr;
   mfg_ctx* c = new mfg_ctx();
   try {
-    if (cfg->precision != MFG_PREC_FP32 && cfg->precision != MFG_PREC_BF16)
+    if (cfg->precision < MFG_PREC_FP32 || cfg->precision > MFG_PREC_BF16X3)
       throw Fail{MFG_ERR_USAGE, "unknown precision " + std::to_string(cfg->precision)};
     c->device = cfg->device;
     c->precision = cfg->precision;
-    c->split = cfg->precision == MFG_PREC_FP32;
+    c->split = cfg->precision != MFG_PREC_BF16;
+    c->fmt = cfg->precision == MFG_PREC_FP32 ? FMT_F16 : FMT_BF16;
     c->profile = cfg->profile != 0;
     CK(cudaSetDevice(c->device));
     int major = 0, minor = 0;
@@ -640,23 +659,20 @@ struct Scratch {
   }
 };
 
-__global__ void split_rows_kernel(const float* src, int rows, int cols, __nv_bfloat16* hi,
-                                  __nv_bfloat16* lo, int ld) {
+__global__ void split_rows_kernel(const float* src, int rows, int cols, uint16_t* hi,
+                                  uint16_t* lo, int ld, int fmt) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)rows * cols) return;
   const int r = (int)(i / cols), c = (int)(i % cols);
-  __nv_bfloat16 h, l;
-  split_bf16(src[i], h, l);
-  hi[(int64_t)r * ld + c] = h;
-  if (lo) lo[(int64_t)r * ld + c] = l;
+  store_split(hi, lo, (size_t)r * ld + c, src[i], fmt, nullptr);
 }
-__global__ void join_rows_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int ld,
-                                 int rows, int cols, float* dst) {
+__global__ void join_rows_kernel(const uint16_t* hi, const uint16_t* lo, int ld,
+                                 int rows, int cols, float* dst, int fmt) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)rows * cols) return;
   const int r = (int)(i / cols), c = (int)(i % cols);
-  float v = __bfloat162float(hi[(int64_t)r * ld + c]);
-  if (lo) v += __bfloat162float(lo[(int64_t)r * ld + c]);
+  float v = load16(hi, (size_t)r * ld + c, fmt);
+  if (lo) v += load16(lo, (size_t)r * ld + c, fmt);
   dst[i] = v;
 }
 
@@ -677,7 +693,8 @@ extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, i
                          const float* A, const float* W, const float* bias,
                          const float* residual, float* out) {
   return guarded([&] {
-    const bool split = precision == MFG_PREC_FP32;
+    const bool split = precision != MFG_PREC_BF16;
+    const int fmt = precision == MFG_PREC_FP32 ? FMT_F16 : FMT_BF16;
     int dev = 0, sms = 148;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -690,28 +707,28 @@ extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, i
     float* dW = s.alloc<float>((size_t)K * N);
     CK(cudaMemcpy(dA, A, (size_t)M * K * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dW, W, (size_t)K * N * 4, cudaMemcpyHostToDevice));
-    auto* ah = s.alloc<__nv_bfloat16>(Mp * Kp);
-    auto* al = split ? s.alloc<__nv_bfloat16>(Mp * Kp) : nullptr;
-    auto* wh = s.alloc<__nv_bfloat16>((size_t)Np * Kp);
-    auto* wl = split ? s.alloc<__nv_bfloat16>((size_t)Np * Kp) : nullptr;
+    auto* ah = s.alloc<uint16_t>(Mp * Kp);
+    auto* al = split ? s.alloc<uint16_t>(Mp * Kp) : nullptr;
+    auto* wh = s.alloc<uint16_t>((size_t)Np * Kp);
+    auto* wl = split ? s.alloc<uint16_t>((size_t)Np * Kp) : nullptr;
     const int64_t tot = (int64_t)M * K;
-    split_rows_kernel<<<(unsigned)((tot + 255) / 256), 256>>>(dA, M, K, ah, al, Kp);
+    split_rows_kernel<<<(unsigned)((tot + 255) / 256), 256>>>(dA, M, K, ah, al, Kp, fmt);
     CK(cudaGetLastError());
-    CK(launch_transpose_split(dW, K, N, wh, wl, Kp, 0, 0));
+    CK(launch_transpose_split(dW, K, N, wh, wl, Kp, 0, fmt, nullptr, 0));
     float* db = s.alloc<float>(Np);
     if (bias) CK(cudaMemcpy(db, bias, N * 4, cudaMemcpyHostToDevice));
     float* dr = s.alloc<float>((size_t)M * Np);
     if (residual)
       CK(cudaMemcpy2D(dr, Np * 4, residual, N * 4, N * 4, M, cudaMemcpyHostToDevice));
     float* d32 = s.alloc<float>((size_t)M * Np);
-    auto* oh = s.alloc<__nv_bfloat16>((size_t)M * Np);
-    auto* ol = split ? s.alloc<__nv_bfloat16>((size_t)M * Np) : nullptr;
+    auto* oh = s.alloc<uint16_t>((size_t)M * Np);
+    auto* ol = split ? s.alloc<uint16_t>((size_t)M * Np) : nullptr;
     CUtensorMap mah, mal, mwh, mwl;
-    if (!make_tmap_bf16(&mah, ah, Mp, Kp, Kp, GEMM_BM, err, sizeof err) ||
-        !make_tmap_bf16(&mwh, wh, Np, Kp, Kp, bn, err, sizeof err))
+    if (!make_tmap_u16(&mah, ah, Mp, Kp, Kp, GEMM_BM, err, sizeof err) ||
+        !make_tmap_u16(&mwh, wh, Np, Kp, Kp, bn, err, sizeof err))
       throw Fail{MFG_ERR_RUNTIME, err};
-    if (split && (!make_tmap_bf16(&mal, al, Mp, Kp, Kp, GEMM_BM, err, sizeof err) ||
-                  !make_tmap_bf16(&mwl, wl, Np, Kp, Kp, bn, err, sizeof err)))
+    if (split && (!make_tmap_u16(&mal, al, Mp, Kp, Kp, GEMM_BM, err, sizeof err) ||
+                  !make_tmap_u16(&mwl, wl, Np, Kp, Kp, bn, err, sizeof err)))
       throw Fail{MFG_ERR_RUNTIME, err};
     GemmArgs g{};
     g.M = M;
@@ -725,13 +742,16 @@ extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, i
     g.out_hi = oh;
     g.out_lo = ol;
     g.ldh = Np;
-    CK(launch_gemm(&mah, split ? &mal : &mah, &mwh, split ? &mwl : &mwh, bn, split, epi, g, sms, 0));
+    g.fmt = fmt;
+    g.ovf = nullptr;
+    CK(launch_gemm(&mah, split ? &mal : &mah, &mwh, split ? &mwl : &mwh, bn, split ? 2 : 1, epi,
+                   g, sms, 0));
     CK(cudaDeviceSynchronize());
     if (epi == EPI_F32 || epi == EPI_F32_RES) {
       CK(cudaMemcpy2D(out, N * 4, d32, Np * 4, N * 4, M, cudaMemcpyDeviceToHost));
     } else {
       float* tmpd = s.alloc<float>((size_t)M * N);
-      join_rows_kernel<<<(unsigned)(((int64_t)M * N + 255) / 256), 256>>>(oh, ol, Np, M, N, tmpd);
+      join_rows_kernel<<<(unsigned)(((int64_t)M * N + 255) / 256), 256>>>(oh, ol, Np, M, N, tmpd, fmt);
       CK(cudaGetLastError());
       CK(cudaMemcpy(out, tmpd, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
     }
@@ -741,7 +761,8 @@ extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, i
 extern "C" int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* cu, int32_t d,
                               int32_t n_heads, const float* qkv, float* ctx_out) {
   return guarded([&] {
-    const bool split = precision == MFG_PREC_FP32;
+    const bool split = precision != MFG_PREC_BF16;
+    const int fmt = precision == MFG_PREC_FP32 ? FMT_F16 : FMT_BF16;
     Scratch s;
     const int T = cu[n_seq];
     const int ldq = pad64(3 * d), ldc = pad64(d);
@@ -754,11 +775,11 @@ extern "C" int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* c
       for (int q = 0; q < cu[i + 1] - cu[i]; q += 64) work.push_back(make_int2(i, q));
     int2* dw = s.alloc<int2>(work.size());
     CK(cudaMemcpy(dw, work.data(), work.size() * sizeof(int2), cudaMemcpyHostToDevice));
-    auto* ch = s.alloc<__nv_bfloat16>((size_t)T * ldc);
-    auto* cl = split ? s.alloc<__nv_bfloat16>((size_t)T * ldc) : nullptr;
-    CK(launch_attention(dq, ldq, d, n_heads, dcu, dw, (int)work.size(), ch, cl, ldc, 0));
+    auto* ch = s.alloc<uint16_t>((size_t)T * ldc);
+    auto* cl = split ? s.alloc<uint16_t>((size_t)T * ldc) : nullptr;
+    CK(launch_attention(dq, ldq, d, n_heads, dcu, dw, (int)work.size(), ch, cl, ldc, fmt, nullptr, 0));
     float* o = s.alloc<float>((size_t)T * d);
-    join_rows_kernel<<<(unsigned)(((int64_t)T * d + 255) / 256), 256>>>(ch, cl, ldc, T, d, o);
+    join_rows_kernel<<<(unsigned)(((int64_t)T * d + 255) / 256), 256>>>(ch, cl, ldc, T, d, o, fmt);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(ctx_out, o, (size_t)T * d * 4, cudaMemcpyDeviceToHost));
@@ -776,7 +797,7 @@ extern "C" int mfgt_layernorm(int32_t T, int32_t d, const float* y, const float*
     CK(cudaMemcpy(dy, y, (size_t)T * d * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dg, g, d * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(db, b, d * 4, cudaMemcpyHostToDevice));
-    CK(launch_layernorm(dy, T, d, d, dg, db, dout, nullptr, nullptr, 0));
+    CK(launch_layernorm(dy, T, d, d, dg, db, dout, nullptr, nullptr, FMT_BF16, nullptr, 0));
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out, dout, (size_t)T * d * 4, cudaMemcpyDeviceToHost));
   });

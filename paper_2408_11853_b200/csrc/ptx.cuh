@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace mfg {
@@ -132,20 +133,48 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(const void* smem_tile) {
   return d;
 }
 
-// Instruction descriptor, kind::f16: bf16 x bf16 -> fp32, both K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
-  return (1u << 4)            // D format f32
-         | (1u << 7)          // A bf16
-         | (1u << 10)         // B bf16
-         | ((N >> 3) << 17)   // N
-         | ((M >> 4) << 24);  // M
+// Instruction descriptor, kind::f16 -> fp32 accumulate, both operands K-major.
+// fmt: FMT_F16 (0) or FMT_BF16 (1) for both A and B.
+__host__ __device__ constexpr uint32_t idesc_f16kind(uint32_t M, uint32_t N, uint32_t fmt) {
+  return (1u << 4)             // D format f32
+         | (fmt << 7)          // A format
+         | (fmt << 10)         // B format
+         | ((N >> 3) << 17)    // N
+         | ((M >> 4) << 24);   // M
 }
 
 // ---------------------------------------------------------------- numerics
-// fp32 -> (hi, lo) bf16 pair with hi + lo == v to ~16 mantissa bits.
-__device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bfloat16& lo) {
-  hi = __float2bfloat16_rn(v);
-  lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+// 16-bit operand formats of the tensor-core path (MMA descriptor encoding).
+constexpr int FMT_F16 = 0;   // IEEE binary16: 11 significant bits, |v| < 65520
+constexpr int FMT_BF16 = 1;  // bfloat16: 8 significant bits, fp32 range
+
+// fp32 -> (hi, lo) pair of 16-bit values with hi + lo ~= v:
+//   fp16 pieces: ~22 significant bits (absolute floor 2^-25), bf16: ~16 bits.
+// Returns false when v does not fit the fp16 range (hi would be inf).
+__device__ __forceinline__ bool split16(float v, int fmt, uint16_t& hi, uint16_t& lo) {
+  if (fmt == FMT_F16) {
+    const __half h = __float2half_rn(v);
+    const float hf = __half2float(h);
+    hi = __half_as_ushort(h);
+    lo = __half_as_ushort(__float2half_rn(v - hf));
+    return isfinite(hf) || !isfinite(v);
+  }
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  hi = __bfloat16_as_ushort(h);
+  lo = __bfloat16_as_ushort(__float2bfloat16_rn(v - __bfloat162float(h)));
+  return true;
+}
+// Store v as hi (and lo, when non-null) at index i; flag fp16 overflow.
+__device__ __forceinline__ void store_split(uint16_t* __restrict__ hi, uint16_t* __restrict__ lo,
+                                            size_t i, float v, int fmt, int* ovf) {
+  uint16_t h, l;
+  if (!split16(v, fmt, h, l) && ovf) atomicOr(ovf, 1);
+  hi[i] = h;
+  if (lo) lo[i] = l;
+}
+__device__ __forceinline__ float load16(const uint16_t* p, size_t i, int fmt) {
+  return fmt == FMT_F16 ? __half2float(__ushort_as_half(p[i]))
+                        : __bfloat162float(__ushort_as_bfloat16(p[i]));
 }
 
 __device__ __forceinline__ float gelu_tanh(float x) {

@@ -7,9 +7,11 @@ Same constructor shape `(container, compute_mode)` and the same
 by `Evaluator`: role-major token ids + cu_seqlens straight from libmfhost.
 
 Precisions (`EvaluatorConfig.precision`):
-  "fp32"  bf16x3 split operands on tcgen05, fp32 accumulate — the parity path
-          (|Δ| ≤ 1e-3 per segment against the fp32 reference)
-  "bf16"  single bf16 MMA per k-step — reported separately with its error stats
+  "fp32"    the parity path: every GEMM operand is an fp16 hi/lo pair (~22
+            significant bits) and each k-step issues 3 tcgen05 MMAs into an fp32
+            TMEM accumulator (|Δ| ≤ 1e-3 per segment against the fp32 reference)
+  "bf16x3"  the same with bf16 pieces (~16 bits, full fp32 range)
+  "bf16"    one bf16 MMA per k-step — reported separately with its error stats
 """
 
 from __future__ import annotations
@@ -25,7 +27,7 @@ from . import native
 from .errors import ContainerError, DeviceError
 from .kinds import N_SEQUENCES, Kind
 
-PRECISIONS = {"fp32": 0, "bf16": 1}
+PRECISIONS = {"fp32": 0, "bf16": 1, "bf16x3": 2}
 
 
 class ComputeMode(enum.Enum):
@@ -67,7 +69,7 @@ class GpuScoringModel:
         self.mode = ComputeMode.parse(compute_mode)
         self.precision = precision or default_precision(self.mode)
         if self.precision not in PRECISIONS:
-            raise ValueError(f"unknown precision {self.precision!r} (known: fp32, bf16)")
+            raise ValueError(f"unknown precision {self.precision!r} (known: fp32, bf16x3, bf16)")
         self._lib = native.gpu()
         cfg = native.MfgConfig(os.fsencode(str(path)), _device_ordinal(device),
                                PRECISIONS[self.precision], int(max_tokens), int(max_records),
