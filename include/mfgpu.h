@@ -64,6 +64,16 @@ int mfg_create(const mfg_config* cfg, mfg_ctx** out);
 int mfg_score_batch(mfg_ctx* ctx, int32_t n_records, int32_t n_roles, const int32_t* ids,
                     const int64_t* cu_seqlens, float* scores_out);
 
+/* Same as mfg_score_batch with DEVICE-resident ids (role-major int32, on the
+ * context's device) and a DEVICE scores_out buffer; cu_seqlens stays on the
+ * host (chunk planning). Out-of-range ids are detected on the device. */
+int mfg_score_device(mfg_ctx* ctx, int32_t n_records, int32_t n_roles, const int32_t* d_ids,
+                     const int64_t* cu_seqlens, float* d_scores_out);
+
+/* Launch every kernel / copy of this context on `stream` (a cudaStream_t of
+ * the context's device; NULL restores the context's own stream). */
+int mfg_set_stream(mfg_ctx* ctx, void* stream);
+
 /* Error of the last failing call on ctx (ctx == NULL: last mfg_create / test
  * call on this thread). Copies a NUL-terminated message into buf. */
 int mfg_last_error(const mfg_ctx* ctx, int32_t* code, char* buf, size_t cap);

@@ -9,21 +9,30 @@ namespace mfg {
 
 // ------------------------------------------------------------------ embedding
 // x_p = E_tok[id_p] + E_pos[p]   (`pkg/src/metricforge/encoder.py:166-168`)
-__global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ pos,
-                             int T, int d, const float* __restrict__ tok,
+// One CTA per sequence (positions restart at every cu_seqlens boundary), one
+// warp per token. Ids outside [0, V) set bit 1 of `flag` (usage error) instead
+// of reading out of bounds (`encoder.py:164-165`).
+__global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ cu,
+                             int V, int d, const float* __restrict__ tok,
                              const float* __restrict__ pe, float* __restrict__ x32, int ld,
                              uint16_t* __restrict__ xh, uint16_t* __restrict__ xl, int fmt,
-                             int* ovf) {
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+                             int* flag) {
+  const int start = cu[blockIdx.x], end = cu[blockIdx.x + 1];
   const int lane = threadIdx.x & 31;
-  if (t >= T) return;
-  const float* a = tok + (size_t)ids[t] * d;
-  const float* b = pe + (size_t)pos[t] * d;
-  const size_t o = (size_t)t * ld;
-  for (int c = lane; c < d; c += 32) {
-    const float v = a[c] + b[c];
-    x32[o + c] = v;
-    if (xh) store_split(xh, xl, o + c, v, fmt, ovf);
+  for (int t = start + (threadIdx.x >> 5); t < end; t += blockDim.x >> 5) {
+    int id = ids[t];
+    if (id < 0 || id >= V) {
+      if (lane == 0) atomicOr(flag, 2);
+      id = 0;
+    }
+    const float* a = tok + (size_t)id * d;
+    const float* b = pe + (size_t)(t - start) * d;
+    const size_t o = (size_t)t * ld;
+    for (int c = lane; c < d; c += 32) {
+      const float v = a[c] + b[c];
+      x32[o + c] = v;
+      if (xh) store_split(xh, xl, o + c, v, fmt, flag);
+    }
   }
 }
 
@@ -265,11 +274,11 @@ __global__ void gather_col0_kernel(const float* __restrict__ out, int ld, int n,
 }
 
 // ------------------------------------------------------------------ launchers
-cudaError_t launch_embed(const int32_t* ids, const int32_t* pos, int T, int d, const float* tok,
-                         const float* pe, float* x32, int ld, uint16_t* xh, uint16_t* xl,
-                         int fmt, int* ovf, cudaStream_t st) {
-  if (T <= 0) return cudaSuccess;
-  embed_kernel<<<(T + 7) / 8, 256, 0, st>>>(ids, pos, T, d, tok, pe, x32, ld, xh, xl, fmt, ovf);
+cudaError_t launch_embed(const int32_t* ids, const int32_t* cu, int nseq, int V, int d,
+                         const float* tok, const float* pe, float* x32, int ld, uint16_t* xh,
+                         uint16_t* xl, int fmt, int* flag, cudaStream_t st) {
+  if (nseq <= 0) return cudaSuccess;
+  embed_kernel<<<nseq, 256, 0, st>>>(ids, cu, V, d, tok, pe, x32, ld, xh, xl, fmt, flag);
   return cudaGetLastError();
 }
 

@@ -7,9 +7,9 @@
 
 namespace mfg {
 
-cudaError_t launch_embed(const int32_t* ids, const int32_t* pos, int T, int d, const float* tok,
-                         const float* pe, float* x32, int ld, uint16_t* xh, uint16_t* xl,
-                         int fmt, int* ovf, cudaStream_t st);
+cudaError_t launch_embed(const int32_t* ids, const int32_t* cu, int nseq, int V, int d,
+                         const float* tok, const float* pe, float* x32, int ld, uint16_t* xh,
+                         uint16_t* xl, int fmt, int* flag, cudaStream_t st);
 cudaError_t launch_layernorm(const float* y, int T, int d, int ld, const float* g, const float* b,
                              float* out32, uint16_t* oh, uint16_t* ol, int fmt, int* ovf,
                              cudaStream_t st);

@@ -80,7 +80,8 @@ struct mfg_ctx {
   Manifest man;
   int kind = 0, n_roles = 0;
   int d = 0, dp = 0, f = 0, fp = 0, H = 0, F = 0, Fp = 0, qkv_ld = 0;
-  cudaStream_t st = nullptr;
+  cudaStream_t st = nullptr;       // stream every launch goes to
+  cudaStream_t own_st = nullptr;   // the one the context created
   std::vector<void*> allocs;
   int64_t device_bytes = 0;
 
@@ -95,9 +96,9 @@ struct mfg_ctx {
   std::vector<Act> ga;  // head hidden-stage outputs
   float* hout = nullptr;
   float* dscores = nullptr;
-  int32_t *d_ids = nullptr, *d_pos = nullptr, *d_cu = nullptr;
+  int32_t *d_ids = nullptr, *d_cu = nullptr;
   int2* d_work = nullptr;
-  int32_t *h_ids = nullptr, *h_pos = nullptr, *h_cu = nullptr;
+  int32_t *h_ids = nullptr, *h_cu = nullptr;
   int2* h_work = nullptr;
   float* h_scores = nullptr;
   int64_t work_cap = 0;
@@ -329,12 +330,10 @@ struct mfg_ctx {
     hout = dalloc<float>((size_t)pad128(cap_records) * head.back().Npad);
     dscores = dalloc<float>(cap_records);
     d_ids = dalloc<int32_t>(cap_tokens);
-    d_pos = dalloc<int32_t>(cap_tokens);
     d_cu = dalloc<int32_t>((size_t)cap_records * n_roles + 1);
     work_cap = cap_tokens / 1 + (int64_t)cap_records * n_roles;
     d_work = dalloc<int2>(work_cap);
     CK(cudaMallocHost(&h_ids, cap_tokens * 4));
-    CK(cudaMallocHost(&h_pos, cap_tokens * 4));
     CK(cudaMallocHost(&h_cu, ((size_t)cap_records * n_roles + 1) * 4));
     CK(cudaMallocHost(&h_work, work_cap * sizeof(int2)));
     CK(cudaMallocHost(&h_scores, cap_records * 4));
@@ -379,18 +378,18 @@ struct mfg_ctx {
   }
 
   // One device chunk: m records, T tokens, role-major packing in h_* staging.
-  void forward_chunk(int m, int64_t T, int64_t n_work, double sum_l2, float* scores_out) {
+  // One device chunk: m records, T tokens; ids already in d_ids (role-major),
+  // cu / work items in the pinned h_* staging. Scores land in dscores[0..m).
+  void forward_chunk(int m, int64_t T, int64_t n_work, double sum_l2) {
     const int nseq = m * n_roles;
-    CK(cudaMemcpyAsync(d_ids, h_ids, T * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_pos, h_pos, T * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d_cu, h_cu, (nseq + 1) * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d_work, h_work, n_work * sizeof(int2), cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(d_ovf, 0, sizeof(int), st));
     const int Ti = (int)T;
     {
       int e = ev_begin();
-      CK(launch_embed(d_ids, d_pos, Ti, d, tok, pos, x32, dp, pre_norm ? nullptr : xa.hi,
-                      pre_norm ? nullptr : xa.lo, fmt, d_ovf, st));
+      CK(launch_embed(d_ids, d_cu, nseq, (int)man.vocab_size, d, tok, pos, x32, dp,
+                      pre_norm ? nullptr : xa.hi, pre_norm ? nullptr : xa.lo, fmt, d_ovf, st));
       ev_end(e, C_EMB, 0, (double)T * d * (8 + 4 + (pre_norm ? 0 : (split ? 4 : 2))));
     }
     for (auto& L : layers) {
@@ -434,16 +433,23 @@ struct mfg_ctx {
       CK(launch_gather_col0(hout, head.back().Npad, m, dscores, st));
       ev_end(e, C_HEAD, 0, (double)m * 8);
     }
-    CK(cudaMemcpyAsync(h_scores, dscores, m * 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h_ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (*h_ovf)
-      throw Fail{MFG_ERR_RUNTIME, "an activation exceeded the fp16 range of the fp32-parity path "
-                                  "(|x| >= 65520); rerun with precision bf16x3"};
-    memcpy(scores_out, h_scores, m * 4);
   }
 
-  void score(int32_t n, int32_t n_roles_in, const int32_t* ids, const int64_t* cu, float* out) {
+  void check_flag() {
+    CK(cudaMemcpyAsync(h_ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (*h_ovf & 2)
+      throw Fail{MFG_ERR_USAGE,
+                 "token id out of range for vocab_size " + std::to_string(man.vocab_size)};
+    if (*h_ovf & 1)
+      throw Fail{MFG_ERR_RUNTIME, "an activation exceeded the fp16 range of the fp32-parity path "
+                                  "(|x| >= 65520); rerun with precision bf16x3"};
+  }
+
+  // ids / out are host pointers (device_io == false) or device pointers (true);
+  // cu_seqlens is always a host array.
+  void score(int32_t n, int32_t n_roles_in, const int32_t* ids, const int64_t* cu, float* out,
+             bool device_io) {
     if (n < 0) throw Fail{MFG_ERR_USAGE, "n_records must be >= 0"};
     if (n_roles_in != n_roles)
       throw Fail{MFG_ERR_USAGE, "model kind '" + man.like + "' scores " + std::to_string(n_roles) +
@@ -458,11 +464,13 @@ struct mfg_ctx {
                                       " exceeds limit " + std::to_string(man.max_position)};
       if (L <= 0) throw Fail{MFG_ERR_USAGE, "cannot pool a row with no tokens"};
     }
-    const int64_t total = cu[nseq];
-    for (int64_t t = 0; t < total; ++t)
-      if (ids[t] < 0 || ids[t] >= man.vocab_size)
-        throw Fail{MFG_ERR_USAGE,
-                   "token id out of range for vocab_size " + std::to_string(man.vocab_size)};
+    if (!device_io) {
+      const int64_t total = cu[nseq];
+      for (int64_t t = 0; t < total; ++t)
+        if (ids[t] < 0 || ids[t] >= man.vocab_size)
+          throw Fail{MFG_ERR_USAGE,
+                     "token id out of range for vocab_size " + std::to_string(man.vocab_size)};
+    }
 
     CK(cudaEventRecord(ev0, st));
     int r0 = 0;
@@ -484,23 +492,38 @@ struct mfg_ctx {
       }
       if (r1 == r0) throw Fail{MFG_ERR_USAGE, "record exceeds device chunk capacity"};
       const int m = r1 - r0;
-      // pack role-major
+      // role-major chunk: cu / work items on the host, ids staged per role
       int64_t at = 0, nw = 0;
       double sum_l2 = 0;
       h_cu[0] = 0;
-      for (int k = 0; k < n_roles; ++k)
-        for (int r = r0; r < r1; ++r) {
-          const int64_t s = (int64_t)k * n + r;
+      for (int k = 0; k < n_roles; ++k) {
+        const int64_t s0 = (int64_t)k * n + r0, s1 = (int64_t)k * n + r1;
+        const int64_t len = cu[s1] - cu[s0];
+        if (device_io)
+          CK(cudaMemcpyAsync(d_ids + at, ids + cu[s0], len * 4, cudaMemcpyDeviceToDevice, st));
+        else
+          memcpy(h_ids + at, ids + cu[s0], len * 4);
+        for (int64_t s = s0; s < s1; ++s) {
           const int64_t L = cu[s + 1] - cu[s];
-          memcpy(h_ids + at, ids + cu[s], L * 4);
-          for (int64_t p = 0; p < L; ++p) h_pos[at + p] = (int32_t)p;
-          const int ls = k * m + (r - r0);
+          const int ls = (int)(k * m + (s - s0));
           for (int64_t q = 0; q < L; q += 64) h_work[nw++] = make_int2(ls, (int)q);
-          at += L;
-          h_cu[ls + 1] = (int32_t)at;
+          h_cu[ls + 1] = (int32_t)(at + (cu[s + 1] - cu[s0]));
           sum_l2 += (double)L * L;
         }
-      forward_chunk(m, T, nw, sum_l2 * man.n_layers, out + r0);
+        at += len;
+      }
+      if (!device_io) CK(cudaMemcpyAsync(d_ids, h_ids, T * 4, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(d_work, h_work, nw * sizeof(int2), cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(d_ovf, 0, sizeof(int), st));
+      forward_chunk(m, T, nw, sum_l2 * man.n_layers);
+      if (device_io) {
+        CK(cudaMemcpyAsync(out + r0, dscores, m * 4, cudaMemcpyDeviceToDevice, st));
+        check_flag();
+      } else {
+        CK(cudaMemcpyAsync(h_scores, dscores, m * 4, cudaMemcpyDeviceToHost, st));
+        check_flag();
+        memcpy(out + r0, h_scores, m * 4);
+      }
       stats.tokens += T;
       stats.chunks += 1;
       r0 = r1;
@@ -519,7 +542,6 @@ struct mfg_ctx {
     if (st) cudaStreamSynchronize(st);
     for (void* p : allocs) cudaFree(p);
     if (h_ids) cudaFreeHost(h_ids);
-    if (h_pos) cudaFreeHost(h_pos);
     if (h_cu) cudaFreeHost(h_cu);
     if (h_work) cudaFreeHost(h_work);
     if (h_scores) cudaFreeHost(h_scores);
@@ -527,7 +549,7 @@ struct mfg_ctx {
     for (auto e : pev) cudaEventDestroy(e);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    if (st) cudaStreamDestroy(st);
+    if (own_st) cudaStreamDestroy(own_st);
   }
 };
 
@@ -558,7 +580,8 @@ extern "C" int mfg_create(const mfg_config* cfg, mfg_ctx** out) {
       throw Fail{MFG_ERR_RUNTIME, "libmfgpu is built for sm_100a (B200); device is sm_" +
                                       std::to_string(major) + std::to_string(minor)};
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
-    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->own_st, cudaStreamNonBlocking));
+    c->st = c->own_st;
     c->build(*cfg);
   } catch (const Fail& f) {
     delete c;
@@ -579,7 +602,7 @@ extern "C" int mfg_score_batch(mfg_ctx* c, int32_t n, int32_t n_roles, const int
   if (!c) return set_global(MFG_ERR_USAGE, "null context");
   try {
     CK(cudaSetDevice(c->device));
-    c->score(n, n_roles, ids, cu, scores);
+    c->score(n, n_roles, ids, cu, scores, false);
   } catch (const Fail& f) {
     c->err_code = f.code;
     c->err_msg = f.msg;
@@ -591,6 +614,34 @@ extern "C" int mfg_score_batch(mfg_ctx* c, int32_t n, int32_t n_roles, const int
   }
   c->err_code = 0;
   c->err_msg.clear();
+  return MFG_OK;
+}
+
+extern "C" int mfg_score_device(mfg_ctx* c, int32_t n, int32_t n_roles, const int32_t* d_ids,
+                                const int64_t* cu, float* d_scores) {
+  if (!c) return set_global(MFG_ERR_USAGE, "null context");
+  try {
+    CK(cudaSetDevice(c->device));
+    c->score(n, n_roles, d_ids, cu, d_scores, true);
+  } catch (const Fail& f) {
+    c->err_code = f.code;
+    c->err_msg = f.msg;
+    return f.code;
+  } catch (const std::exception& e) {
+    c->err_code = MFG_ERR_RUNTIME;
+    c->err_msg = e.what();
+    return MFG_ERR_RUNTIME;
+  }
+  c->err_code = 0;
+  c->err_msg.clear();
+  return MFG_OK;
+}
+
+extern "C" int mfg_set_stream(mfg_ctx* c, void* stream) {
+  if (!c) return set_global(MFG_ERR_USAGE, "null context");
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->st);
+  c->st = stream ? (cudaStream_t)stream : c->own_st;
   return MFG_OK;
 }
 

@@ -108,6 +108,22 @@ class GpuScoringModel:
                 raise (ValueError if rc == 2 else ContainerError if rc == 3 else DeviceError)(msg)
         return out
 
+    def score_device(self, ids_ptr, cu_seqlens, n_records, scores_ptr):
+        """Device-resident variant: ids_ptr / scores_ptr are device addresses
+        (int32 role-major ids, float32[n] out); cu_seqlens is a host int64 array."""
+        cu = np.ascontiguousarray(cu_seqlens, dtype=np.int64)
+        with self._lock:
+            rc = self._lib.mfg_score_device(self._h, int(n_records), self.n_roles,
+                                            C.c_void_p(ids_ptr), native.ptr(cu, C.c_int64),
+                                            C.c_void_p(scores_ptr))
+            if rc != 0:
+                _, msg = native.last_error(self._h)
+                raise (ValueError if rc == 2 else ContainerError if rc == 3 else DeviceError)(msg)
+
+    def set_stream(self, stream_handle):
+        """Route every launch to an external cudaStream_t (int handle; 0 = own)."""
+        self._lib.mfg_set_stream(self._h, C.c_void_p(stream_handle or None))
+
     def score_records(self, encoded_records) -> np.ndarray:
         """`encoded_records`: per record, the TokenSequence list of encode_fields
         for this model's kind (role order). Returns float32 scores in order."""

@@ -96,6 +96,10 @@ def gpu():
             lib.mfg_create.restype = C.c_int
             lib.mfg_score_batch.argtypes = [C.c_void_p, i32, i32, i32p, i64p, f32p]
             lib.mfg_score_batch.restype = C.c_int
+            lib.mfg_score_device.argtypes = [C.c_void_p, i32, i32, C.c_void_p, i64p, C.c_void_p]
+            lib.mfg_score_device.restype = C.c_int
+            lib.mfg_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+            lib.mfg_set_stream.restype = C.c_int
             lib.mfg_last_error.argtypes = [C.c_void_p, i32p, C.c_char_p, C.c_size_t]
             lib.mfg_last_error.restype = C.c_int
             lib.mfg_destroy.argtypes = [C.c_void_p]
