@@ -18,9 +18,10 @@ int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, int32_t K, c
               const float* W, const float* bias, const float* residual, float* out);
 
 /* ctx[T][d] = attention of packed qkv[T][3d] (q | k | v per row), sequences given by
- * cu[n_seq + 1], heads = n_heads, scale 1/sqrt(d/heads). */
+ * cu[n_seq + 1], heads = n_heads, scale 1/sqrt(d/heads). use_tc = 1 routes sequences
+ * of <= 128 tokens with d_head 64 to the tcgen05 kernel, 0 forces the SIMT kernel. */
 int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* cu, int32_t d,
-                   int32_t n_heads, const float* qkv, float* ctx_out);
+                   int32_t n_heads, const float* qkv, float* ctx_out, int32_t use_tc);
 
 /* out[T][d] = LayerNorm(y) with gain g and bias b (eps 1e-5). */
 int mfgt_layernorm(int32_t T, int32_t d, const float* y, const float* g, const float* b,

@@ -81,6 +81,7 @@ static cudaError_t run_epi(int epi, const CUtensorMap* ah, const CUtensorMap* al
     case EPI_F32_RES: return run<BN, SPLIT, EPI_F32_RES>(ah, al, bh, bl, a, num_sms, st);
     case EPI_GELU_SPLIT: return run<BN, SPLIT, EPI_GELU_SPLIT>(ah, al, bh, bl, a, num_sms, st);
     case EPI_TANH_SPLIT: return run<BN, SPLIT, EPI_TANH_SPLIT>(ah, al, bh, bl, a, num_sms, st);
+    case EPI_SPLIT: return run<BN, SPLIT, EPI_SPLIT>(ah, al, bh, bl, a, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -7,8 +7,9 @@
 // and fuses the ops that follow each affine into the epilogue:
 //   EPI_F32        out = acc + bias                         (QKV, head output)
 //   EPI_F32_RES    out = acc + bias + residual              (O-proj, FFN2)
-//   EPI_GELU_SPLIT out = gelu_tanh(acc + bias) -> bf16 hi/lo (FFN1, `encoder.py:149-151`)
-//   EPI_TANH_SPLIT out = tanh(acc + bias)      -> bf16 hi/lo (head hidden stages, `:190-196`)
+//   EPI_GELU_SPLIT out = gelu_tanh(acc + bias) -> hi/lo pieces (FFN1, `encoder.py:149-151`)
+//   EPI_TANH_SPLIT out = tanh(acc + bias)      -> hi/lo pieces (head hidden stages, `:190-196`)
+//   EPI_SPLIT      out = acc + bias            -> hi/lo pieces (Q|K|V for attention)
 //
 // SPLIT=true: A = A_hi + A_lo and B = B_hi + B_lo are pairs of 16-bit pieces
 // and every k-step issues  D += A_hi·B_hi + A_lo·B_hi + A_hi·B_lo  into one fp32
@@ -16,17 +17,22 @@
 // ~22 significant bits; with bf16 pieces ("bf16x3") ~16 bits over the fp32 range.
 // SPLIT=false is the plain one-MMA-per-k-step path.
 //
-// Roles (256 threads): warp0 lane0 = TMA producer, warp1 lane0 = MMA issuer,
-// warp2 = TMEM allocator, warps4-7 = epilogue (warp w owns TMEM lanes
-// 32*(w%4)..+31 = tile rows). Two TMEM accumulators let the epilogue of tile
-// i overlap the MMAs of tile i+1. Tiles are assigned round-robin to a
-// persistent grid of <= #SM CTAs.
+// Roles (384 threads): warp0 lane0 = TMA producer, warp1 lane0 = MMA issuer,
+// warp2 = TMEM allocator, warps 4-11 = epilogue. Epilogue warp w reads TMEM
+// lanes 32*(w%4)..+31 (= tile rows) and every other 32-column chunk; each chunk
+// is transposed through shared memory so global traffic is float4 per lane,
+// 4 full 128-byte row segments per warp instruction, with the residual chunk
+// prefetched before the math. Two TMEM accumulators let the epilogue of tile i
+// overlap the MMAs of tile i+1. Tiles are assigned round-robin to a persistent
+// grid of <= #SM CTAs.
 #pragma once
 #include "ptx.cuh"
 
 namespace mfg {
 
-enum EpiMode : int { EPI_F32 = 0, EPI_F32_RES = 1, EPI_GELU_SPLIT = 2, EPI_TANH_SPLIT = 3 };
+enum EpiMode : int {
+  EPI_F32 = 0, EPI_F32_RES = 1, EPI_GELU_SPLIT = 2, EPI_TANH_SPLIT = 3, EPI_SPLIT = 4
+};
 
 struct GemmArgs {
   int M, N, K;               // M real rows; N, K padded (N % BN == 0, K % 64 == 0)
@@ -44,9 +50,10 @@ struct GemmArgs {
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_THREADS = 384;
+constexpr int GEMM_EPI_WARPS = 8;
 constexpr int GEMM_SMEM_LIMIT = 232448;  // 227 KB opt-in dynamic smem
-constexpr int GEMM_EPI_BYTES = 4 * 32 * 33 * 4;
+constexpr int GEMM_EPI_BYTES = GEMM_EPI_WARPS * 32 * 33 * 4;
 constexpr int GEMM_BAR_BYTES = 256;
 
 template <int BN, bool SPLIT>
@@ -99,7 +106,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], GEMM_EPI_WARPS);
     }
     fence_mbar_init();
   }
@@ -184,38 +191,70 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    const int q = warp & 3;  // TMEM lane quarter == tile row block
-    float* buf = epi_buf + q * 32 * 33;
+    const int ew = warp - 4;       // 0..7
+    const int q = warp & 3;        // TMEM lane quarter == 32-row block of the tile
+    const int half = ew >> 2;      // which alternate 32-column chunks this warp owns
+    float* buf = epi_buf + ew * 32 * 33;
+    const int cg = lane & 7;       // transposed phase: 4 columns 4*cg..4*cg+3
+    const int rs = lane >> 3;      // row sub-index 0..3
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const int m0 = (tile / num_n) * GEMM_BM;
       const int n0 = (tile % num_n) * BN;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
       const int row0 = m0 + q * 32;
       const int rows = min(32, args.M - row0);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = half * 32; c < BN; c += 64) {
+        const int col = n0 + c + 4 * cg;
+        // prefetch this chunk's residual (8 x float4 per lane) before touching TMEM
+        float4 res[8];
+        if (EPI == EPI_F32_RES) {
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int r = it * 4 + rs;
+            res[it] = r < rows ? *reinterpret_cast<const float4*>(
+                                     args.residual + (size_t)(row0 + r) * args.ldr + col)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
         float v[32];
         tmem_ld_32x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
 #pragma unroll
         for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = v[i];
         __syncwarp();
-        const int col = n0 + c + lane;
-        const float b = args.bias[col];
-#pragma unroll 4
-        for (int r = 0; r < rows; ++r) {
-          const size_t row = (size_t)(row0 + r);
-          float x = buf[r * 33 + lane] + b;
-          if (EPI == EPI_F32) {
-            args.out_f32[row * args.ldo + col] = x;
-          } else if (EPI == EPI_F32_RES) {
-            x += args.residual[row * args.ldr + col];
-            args.out_f32[row * args.ldo + col] = x;
-          } else {
-            x = (EPI == EPI_GELU_SPLIT) ? gelu_tanh(x) : tanhf(x);
-            store_split(args.out_hi, args.out_lo, row * args.ldh + col, x, args.fmt, args.ovf);
+        const float4 b = *reinterpret_cast<const float4*>(args.bias + col);
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int r = it * 4 + rs;
+          if (r < rows) {
+            const float* src = buf + r * 33 + 4 * cg;
+            float x[4] = {src[0] + b.x, src[1] + b.y, src[2] + b.z, src[3] + b.w};
+            const size_t o = (size_t)(row0 + r);
+            if (EPI == EPI_F32 || EPI == EPI_F32_RES) {
+              if (EPI == EPI_F32_RES) {
+                x[0] += res[it].x; x[1] += res[it].y; x[2] += res[it].z; x[3] += res[it].w;
+              }
+              *reinterpret_cast<float4*>(args.out_f32 + o * args.ldo + col) =
+                  make_float4(x[0], x[1], x[2], x[3]);
+            } else {
+              uint16_t h[4], l[4];
+              bool ok = true;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float y = (EPI == EPI_GELU_SPLIT) ? gelu_tanh(x[j])
+                                : (EPI == EPI_TANH_SPLIT) ? tanhf(x[j]) : x[j];
+                ok &= split16(y, args.fmt, h[j], l[j]);
+              }
+              if (!ok && args.ovf) atomicOr(args.ovf, 1);
+              *reinterpret_cast<uint2*>(args.out_hi + o * args.ldh + col) =
+                  make_uint2(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16));
+              if (args.out_lo)
+                *reinterpret_cast<uint2*>(args.out_lo + o * args.ldh + col) =
+                    make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
+            }
           }
         }
         __syncwarp();

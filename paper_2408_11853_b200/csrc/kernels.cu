@@ -79,27 +79,54 @@ __global__ void layernorm_kernel(const float* __restrict__ y, int T, int d, int 
 }
 
 // ------------------------------------------------------------------ attention
-// Exact (non-approximate) fp32 masked-softmax attention per (sequence, head),
+// Exact fp32 masked-softmax attention per (sequence, head, 64-query block),
 // flash-style over 64-key blocks (`encoder.py:132-147`, `masked_softmax` 60-66).
 // PAD keys never exist in the packed layout; keys past the sequence end inside
 // the last block get -inf and therefore exactly zero weight.
-// CTA = 128 threads = 16 row groups x 8 column groups; a thread owns 4 query
-// rows x 8 keys of S and 4 rows x DHC output columns (column = cg + 8*i).
+// CTA = 128 threads = 16 row groups (rg) x 8 column groups (cg). A thread owns
+// 4 query rows; in S it owns keys cg + 8j (j < 8), in O the columns
+// 32g + 4cg + {0..3}. Shared-memory operands are read as float4 (row strides
+// are multiples of 4 floats; conflict-free across the 8 column groups).
 constexpr int ATT_BQ = 64, ATT_BK = 64, ATT_THREADS = 128;
+constexpr int ATT_PSTR = ATT_BK + 4;
+
+template <int DHC>
+struct AttCfg {
+  static constexpr int DHMAX = DHC * 8;          // padded head dim
+  static constexpr int STR = DHMAX + 4;          // Q/K/V row stride (floats)
+  static constexpr int G = (DHMAX + 31) / 32;    // float4 column groups per thread in O
+  static constexpr size_t SMEM = sizeof(float) * (3 * 64 * STR + 64 * ATT_PSTR);
+};
+
+// rows x dh fp32 tile = hi + lo of the QKV GEMM's 16-bit output pieces
+__device__ __forceinline__ void att_load_tile(float* dst, int str, const uint16_t* hi,
+                                              const uint16_t* lo, int ldq, int nrows, int dh,
+                                              int dhmax, int tid, int fmt) {
+  for (int i = tid; i < 64 * dhmax; i += ATT_THREADS) {
+    const int r = i / dhmax, c = i % dhmax;
+    float v = 0.f;
+    if (r < nrows && c < dh) {
+      const size_t o = (size_t)r * ldq + c;
+      v = load16(hi, o, fmt);
+      if (lo) v += load16(lo, o, fmt);
+    }
+    dst[r * str + c] = v;
+  }
+}
 
 template <int DHC>
 __global__ void __launch_bounds__(ATT_THREADS)
-    attention_kernel(const float* __restrict__ qkv, int ldq, int d, int dh, float scale,
-                     const int32_t* __restrict__ cu, const int2* __restrict__ work,
+    attention_kernel(const uint16_t* __restrict__ qh, const uint16_t* __restrict__ ql, int ldq,
+                     int d, int dh, float scale, const int32_t* __restrict__ cu,
+                     const int2* __restrict__ work,
                      uint16_t* __restrict__ ch, uint16_t* __restrict__ cl, int ldc, int fmt,
                      int* ovf) {
-  constexpr int DHMAX = DHC * 8;
-  constexpr int STR = DHMAX + 1;
-  extern __shared__ float sm[];
-  float* Qs = sm;                   // [BQ][STR]
-  float* Ks = Qs + ATT_BQ * STR;    // [BK][STR]
-  float* Vs = Ks + ATT_BK * STR;    // [BK][STR]
-  float* Ps = Vs + ATT_BK * STR;    // [BQ][BK+1]
+  using C = AttCfg<DHC>;
+  extern __shared__ float4 sm4[];
+  float* Qs = reinterpret_cast<float*>(sm4);
+  float* Ks = Qs + 64 * C::STR;
+  float* Vs = Ks + 64 * C::STR;
+  float* Ps = Vs + 64 * C::STR;
 
   const int2 w = work[blockIdx.x];
   const int seq = w.x, q0 = w.y;
@@ -109,33 +136,26 @@ __global__ void __launch_bounds__(ATT_THREADS)
   const int nq = min(ATT_BQ, L - q0);
   const int tid = threadIdx.x;
   const int rg = tid >> 3, cg = tid & 7;
+  const int dh4 = (dh + 3) & ~3;
+  const size_t qo = (size_t)(start + q0) * ldq + h * dh;
+  att_load_tile(Qs, C::STR, qh + qo, ql ? ql + qo : nullptr, ldq, nq, dh, C::DHMAX, tid, fmt);
 
-  const float* qbase = qkv + (size_t)start * ldq + h * dh;
-  for (int i = tid; i < ATT_BQ * DHMAX; i += ATT_THREADS) {
-    const int r = i / DHMAX, c = i % DHMAX;
-    Qs[r * STR + c] = (r < nq && c < dh) ? qbase[(size_t)(q0 + r) * ldq + c] : 0.f;
-  }
-
-  float m[4], l[4], o[4][DHC];
+  float m[4], l[4], o[4][C::G * 4];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     m[a] = -INFINITY;
     l[a] = 0.f;
 #pragma unroll
-    for (int i = 0; i < DHC; ++i) o[a][i] = 0.f;
+    for (int i = 0; i < C::G * 4; ++i) o[a][i] = 0.f;
   }
 
   for (int k0 = 0; k0 < L; k0 += ATT_BK) {
     const int nk = min(ATT_BK, L - k0);
     __syncthreads();
-    const float* kb = qkv + (size_t)(start + k0) * ldq + d + h * dh;
-    const float* vb = kb + d;
-    for (int i = tid; i < ATT_BK * DHMAX; i += ATT_THREADS) {
-      const int r = i / DHMAX, c = i % DHMAX;
-      const bool ok = r < nk && c < dh;
-      Ks[r * STR + c] = ok ? kb[(size_t)r * ldq + c] : 0.f;
-      Vs[r * STR + c] = ok ? vb[(size_t)r * ldq + c] : 0.f;
-    }
+    const size_t ko = (size_t)(start + k0) * ldq + d + h * dh;
+    att_load_tile(Ks, C::STR, qh + ko, ql ? ql + ko : nullptr, ldq, nk, dh, C::DHMAX, tid, fmt);
+    att_load_tile(Vs, C::STR, qh + ko + d, ql ? ql + ko + d : nullptr, ldq, nk, dh, C::DHMAX, tid,
+                  fmt);
     __syncthreads();
 
     float s[4][8];
@@ -143,16 +163,23 @@ __global__ void __launch_bounds__(ATT_THREADS)
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int j = 0; j < 8; ++j) s[a][j] = 0.f;
-    for (int c = 0; c < dh; ++c) {
-      float qv[4], kv[8];
+    for (int c = 0; c < dh4; c += 4) {
+      float4 qv[4], kv[8];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) qv[a] = Qs[(rg * 4 + a) * STR + c];
+      for (int a = 0; a < 4; ++a)
+        qv[a] = *reinterpret_cast<const float4*>(Qs + (rg * 4 + a) * C::STR + c);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) kv[j] = Ks[(cg + 8 * j) * STR + c];
+      for (int j = 0; j < 8; ++j)
+        kv[j] = *reinterpret_cast<const float4*>(Ks + (cg + 8 * j) * C::STR + c);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) s[a][j] = fmaf(qv[a], kv[j], s[a][j]);
+        for (int j = 0; j < 8; ++j) {
+          s[a][j] = fmaf(qv[a].x, kv[j].x, s[a][j]);
+          s[a][j] = fmaf(qv[a].y, kv[j].y, s[a][j]);
+          s[a][j] = fmaf(qv[a].z, kv[j].z, s[a][j]);
+          s[a][j] = fmaf(qv[a].w, kv[j].w, s[a][j]);
+        }
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
@@ -172,7 +199,7 @@ __global__ void __launch_bounds__(ATT_THREADS)
       for (int j = 0; j < 8; ++j) {
         const float p = expf(s[a][j] - mn);
         sum += p;
-        Ps[(rg * 4 + a) * (ATT_BK + 1) + cg + 8 * j] = p;
+        Ps[(rg * 4 + a) * ATT_PSTR + cg + 8 * j] = p;
       }
       sum += __shfl_xor_sync(0xffffffffu, sum, 1);
       sum += __shfl_xor_sync(0xffffffffu, sum, 2);
@@ -180,19 +207,33 @@ __global__ void __launch_bounds__(ATT_THREADS)
       l[a] = l[a] * corr + sum;
       m[a] = mn;
 #pragma unroll
-      for (int i = 0; i < DHC; ++i) o[a][i] *= corr;
+      for (int i = 0; i < C::G * 4; ++i) o[a][i] *= corr;
     }
     __syncthreads();
-    for (int j = 0; j < nk; ++j) {
-      float pv[4], vv[DHC];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) pv[a] = Ps[(rg * 4 + a) * (ATT_BK + 1) + j];
-#pragma unroll
-      for (int i = 0; i < DHC; ++i) vv[i] = Vs[j * STR + cg + 8 * i];
+    const int nk4 = (nk + 3) & ~3;  // P is exactly 0 for keys >= nk
+    for (int j = 0; j < nk4; j += 4) {
+      float4 pv[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
+        pv[a] = *reinterpret_cast<const float4*>(Ps + (rg * 4 + a) * ATT_PSTR + j);
 #pragma unroll
-        for (int i = 0; i < DHC; ++i) o[a][i] = fmaf(pv[a], vv[i], o[a][i]);
+      for (int jj = 0; jj < 4; ++jj) {
+#pragma unroll
+        for (int g = 0; g < C::G; ++g) {
+          const int c = 32 * g + 4 * cg;
+          if (c < C::DHMAX) {
+            const float4 vv = *reinterpret_cast<const float4*>(Vs + (j + jj) * C::STR + c);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              const float p = jj == 0 ? pv[a].x : jj == 1 ? pv[a].y : jj == 2 ? pv[a].z : pv[a].w;
+              o[a][4 * g + 0] = fmaf(p, vv.x, o[a][4 * g + 0]);
+              o[a][4 * g + 1] = fmaf(p, vv.y, o[a][4 * g + 1]);
+              o[a][4 * g + 2] = fmaf(p, vv.z, o[a][4 * g + 2]);
+              o[a][4 * g + 3] = fmaf(p, vv.w, o[a][4 * g + 3]);
+            }
+          }
+        }
+      }
     }
   }
 
@@ -203,10 +244,12 @@ __global__ void __launch_bounds__(ATT_THREADS)
     const float inv = 1.0f / l[a];
     const size_t ob = (size_t)(start + q0 + r) * ldc + h * dh;
 #pragma unroll
-    for (int i = 0; i < DHC; ++i) {
-      const int c = cg + 8 * i;
-      if (c < dh) store_split(ch, cl, ob + c, o[a][i] * inv, fmt, ovf);
-    }
+    for (int g = 0; g < C::G; ++g)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int c = 32 * g + 4 * cg + e;
+        if (c < dh) store_split(ch, cl, ob + c, o[a][4 * g + e] * inv, fmt, ovf);
+      }
   }
 }
 
@@ -300,21 +343,22 @@ cudaError_t launch_layernorm(const float* y, int T, int d, int ld, const float* 
 }
 
 template <int DHC>
-static cudaError_t att_launch(const float* qkv, int ldq, int d, int dh, float scale,
+static cudaError_t att_launch(const uint16_t* qh, const uint16_t* ql, int ldq, int d, int dh,
+                              float scale,
                               const int32_t* cu, const int2* work, int n_work, int heads,
                               uint16_t* ch, uint16_t* cl, int ldc, int fmt, int* ovf,
                               cudaStream_t st) {
-  constexpr int STR = DHC * 8 + 1;
-  const size_t smem = sizeof(float) * (3 * 64 * STR + 64 * 65);
+  const size_t smem = AttCfg<DHC>::SMEM;
   cudaFuncSetAttribute(attention_kernel<DHC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  attention_kernel<DHC><<<dim3(n_work, heads), ATT_THREADS, smem, st>>>(qkv, ldq, d, dh, scale,
+  attention_kernel<DHC><<<dim3(n_work, heads), ATT_THREADS, smem, st>>>(qh, ql, ldq, d, dh, scale,
                                                                          cu, work, ch, cl, ldc,
                                                                          fmt, ovf);
   return cudaGetLastError();
 }
 
-cudaError_t launch_attention(const float* qkv, int ldq, int d, int heads, const int32_t* cu,
+cudaError_t launch_attention(const uint16_t* qh, const uint16_t* ql, int ldq, int d, int heads,
+                             const int32_t* cu,
                              const int2* work, int n_work, uint16_t* ch, uint16_t* cl,
                              int ldc, int fmt, int* ovf, cudaStream_t st) {
   if (n_work <= 0) return cudaSuccess;
@@ -322,7 +366,7 @@ cudaError_t launch_attention(const float* qkv, int ldq, int d, int heads, const 
   const float scale = 1.0f / sqrtf((float)d / (float)heads);
   const int dhc = (dh + 7) / 8;
 #define ATT_CASE(V) \
-  if (dhc <= V) return att_launch<V>(qkv, ldq, d, dh, scale, cu, work, n_work, heads, ch, cl, ldc, fmt, ovf, st);
+  if (dhc <= V) return att_launch<V>(qh, ql, ldq, d, dh, scale, cu, work, n_work, heads, ch, cl, ldc, fmt, ovf, st);
   ATT_CASE(1) ATT_CASE(2) ATT_CASE(4) ATT_CASE(8) ATT_CASE(10) ATT_CASE(12) ATT_CASE(16)
 #undef ATT_CASE
   return cudaErrorInvalidValue;

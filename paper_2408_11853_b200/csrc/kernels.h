@@ -13,9 +13,19 @@ cudaError_t launch_embed(const int32_t* ids, const int32_t* cu, int nseq, int V,
 cudaError_t launch_layernorm(const float* y, int T, int d, int ld, const float* g, const float* b,
                              float* out32, uint16_t* oh, uint16_t* ol, int fmt, int* ovf,
                              cudaStream_t st);
-cudaError_t launch_attention(const float* qkv, int ldq, int d, int heads, const int32_t* cu,
+// SIMT fp32 attention over (sequence, 64-query block) work items; Q|K|V read as
+// hi(+lo) 16-bit pieces [T][ldq].
+cudaError_t launch_attention(const uint16_t* qh, const uint16_t* ql, int ldq, int d, int heads,
+                             const int32_t* cu,
                              const int2* work, int n_work, uint16_t* ch, uint16_t* cl,
                              int ldc, int fmt, int* ovf, cudaStream_t st);
+// tcgen05 attention, one CTA per (listed sequence, head); L <= 128, d_head == 64.
+// Maps: Q|K|V hi/lo [T][ldq] with box {64 cols, 128 rows} and {64, 64}.
+cudaError_t launch_attention_tc(const CUtensorMap* mh128, const CUtensorMap* ml128,
+                                const CUtensorMap* mh64, const CUtensorMap* ml64, bool split,
+                                const int32_t* cu, const int32_t* seqs, int n_seqs, int heads,
+                                int d, int fmt, uint16_t* ch, uint16_t* cl, int ldc, int* ovf,
+                                cudaStream_t st);
 cudaError_t launch_features(const float* x, int ld, int d, int kind, const int32_t* cu, int n,
                             uint16_t* fh, uint16_t* fl, int ldf, int fmt, int* ovf,
                             cudaStream_t st);

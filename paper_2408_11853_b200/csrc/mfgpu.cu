@@ -91,8 +91,11 @@ struct mfg_ctx {
 
   int64_t cap_tokens = 0;
   int cap_records = 0;
-  float *x32 = nullptr, *y32 = nullptr, *qkv = nullptr;
-  Act xa, ca, ha, fa;
+  float *x32 = nullptr, *y32 = nullptr;
+  Act xa, ca, ha, fa, qa;          // qa: Q|K|V pieces [T][qkv_ld]
+  CUtensorMap qmh64{}, qml64{};     // Q|K|V maps with 64-row boxes (short sequences)
+  bool att_tc = false;              // tcgen05 attention usable (d_head == 64)
+  int32_t *d_short = nullptr, *h_short = nullptr;
   std::vector<Act> ga;  // head hidden-stage outputs
   float* hout = nullptr;
   float* dscores = nullptr;
@@ -320,7 +323,15 @@ struct mfg_ctx {
     cap_records = cfg.max_records > 0 ? cfg.max_records : 4096;
     x32 = dalloc<float>((size_t)cap_tokens * dp);
     y32 = dalloc<float>((size_t)cap_tokens * dp);
-    qkv = dalloc<float>((size_t)cap_tokens * qkv_ld);
+    make_act(qa, cap_tokens, qkv_ld);
+    {
+      char err[256];
+      if (!make_tmap_u16(&qmh64, qa.hi, qa.rows, qa.ld, qa.ld, 64, err, sizeof err))
+        throw Fail{MFG_ERR_RUNTIME, err};
+      if (split && !make_tmap_u16(&qml64, qa.lo, qa.rows, qa.ld, qa.ld, 64, err, sizeof err))
+        throw Fail{MFG_ERR_RUNTIME, err};
+    }
+    att_tc = (d / H == 64) && (d % 64 == 0);
     make_act(xa, cap_tokens, dp);
     make_act(ca, cap_tokens, dp);
     make_act(ha, cap_tokens, fp);
@@ -331,6 +342,8 @@ struct mfg_ctx {
     dscores = dalloc<float>(cap_records);
     d_ids = dalloc<int32_t>(cap_tokens);
     d_cu = dalloc<int32_t>((size_t)cap_records * n_roles + 1);
+    d_short = dalloc<int32_t>((size_t)cap_records * n_roles);
+    CK(cudaMallocHost(&h_short, (size_t)cap_records * n_roles * 4));
     work_cap = cap_tokens / 1 + (int64_t)cap_records * n_roles;
     d_work = dalloc<int2>(work_cap);
     CK(cudaMallocHost(&h_ids, cap_tokens * 4));
@@ -380,9 +393,11 @@ struct mfg_ctx {
   // One device chunk: m records, T tokens, role-major packing in h_* staging.
   // One device chunk: m records, T tokens; ids already in d_ids (role-major),
   // cu / work items in the pinned h_* staging. Scores land in dscores[0..m).
-  void forward_chunk(int m, int64_t T, int64_t n_work, double sum_l2) {
+  void forward_chunk(int m, int64_t T, int64_t n_work, int n_short, double sum_l2) {
     const int nseq = m * n_roles;
     CK(cudaMemcpyAsync(d_cu, h_cu, (nseq + 1) * 4, cudaMemcpyHostToDevice, st));
+    if (n_short > 0)
+      CK(cudaMemcpyAsync(d_short, h_short, n_short * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d_work, h_work, n_work * sizeof(int2), cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(d_ovf, 0, sizeof(int), st));
     const int Ti = (int)T;
@@ -394,12 +409,19 @@ struct mfg_ctx {
     }
     for (auto& L : layers) {
       if (pre_norm) layernorm(x32, Ti, L.g1, L.b1, nullptr, &xa);
-      gemm(xa, L.qkv, Ti, EPI_F32, C_QKV, nullptr, 0, qkv, qkv_ld, nullptr);
+      gemm(xa, L.qkv, Ti, EPI_SPLIT, C_QKV, nullptr, 0, nullptr, 0, &qa);
       {
+        const double bytes = (double)T * d * 4 * (split ? 4 : 2);
         int e = ev_begin();
-        CK(launch_attention(qkv, qkv_ld, d, H, d_cu, d_work, (int)n_work, ca.hi, ca.lo, ca.ld,
-                            fmt, d_ovf, st));
-        ev_end(e, C_ATT, 4.0 * sum_l2 * d, (double)T * d * (12 + (split ? 4 : 2)));
+        if (n_short > 0)
+          CK(launch_attention_tc(&qa.mh, split ? &qa.ml : &qa.mh, &qmh64, split ? &qml64 : &qmh64,
+                                 split, d_cu, d_short, n_short, H, d, fmt, ca.hi, ca.lo, ca.ld,
+                                 d_ovf, st));
+        if (n_work > 0)
+          CK(launch_attention(qa.hi, qa.lo, qa.ld, d, H, d_cu, d_work, (int)n_work, ca.hi, ca.lo,
+                              ca.ld, fmt, d_ovf, st));
+        ev_end(e, C_ATT, 4.0 * sum_l2 * d, bytes);
+        if (n_short > 0 && n_work > 0) stats.kernel_launches += 1;
       }
       gemm(ca, L.o, Ti, EPI_F32_RES, C_O, x32, dp, y32, dp, nullptr);
       if (!pre_norm) {
@@ -494,6 +516,7 @@ struct mfg_ctx {
       const int m = r1 - r0;
       // role-major chunk: cu / work items on the host, ids staged per role
       int64_t at = 0, nw = 0;
+      int ns = 0;
       double sum_l2 = 0;
       h_cu[0] = 0;
       for (int k = 0; k < n_roles; ++k) {
@@ -506,16 +529,20 @@ struct mfg_ctx {
         for (int64_t s = s0; s < s1; ++s) {
           const int64_t L = cu[s + 1] - cu[s];
           const int ls = (int)(k * m + (s - s0));
-          for (int64_t q = 0; q < L; q += 64) h_work[nw++] = make_int2(ls, (int)q);
+          if (att_tc && L <= 128)
+            h_short[ns++] = ls;
+          else
+            for (int64_t q = 0; q < L; q += 64) h_work[nw++] = make_int2(ls, (int)q);
           h_cu[ls + 1] = (int32_t)(at + (cu[s + 1] - cu[s0]));
           sum_l2 += (double)L * L;
         }
         at += len;
       }
       if (!device_io) CK(cudaMemcpyAsync(d_ids, h_ids, T * 4, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(d_work, h_work, nw * sizeof(int2), cudaMemcpyHostToDevice, st));
+      if (nw > 0)
+        CK(cudaMemcpyAsync(d_work, h_work, nw * sizeof(int2), cudaMemcpyHostToDevice, st));
       CK(cudaMemsetAsync(d_ovf, 0, sizeof(int), st));
-      forward_chunk(m, T, nw, sum_l2 * man.n_layers);
+      forward_chunk(m, T, nw, ns, sum_l2);
       if (device_io) {
         CK(cudaMemcpyAsync(out + r0, dscores, m * 4, cudaMemcpyDeviceToDevice, st));
         check_flag();
@@ -545,6 +572,7 @@ struct mfg_ctx {
     if (h_cu) cudaFreeHost(h_cu);
     if (h_work) cudaFreeHost(h_work);
     if (h_scores) cudaFreeHost(h_scores);
+    if (h_short) cudaFreeHost(h_short);
     if (h_ovf) cudaFreeHost(h_ovf);
     for (auto e : pev) cudaEventDestroy(e);
     if (ev0) cudaEventDestroy(ev0);
@@ -810,25 +838,57 @@ extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, i
 }
 
 extern "C" int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* cu, int32_t d,
-                              int32_t n_heads, const float* qkv, float* ctx_out) {
+                              int32_t n_heads, const float* qkv, float* ctx_out, int32_t use_tc) {
   return guarded([&] {
     const bool split = precision != MFG_PREC_BF16;
     const int fmt = precision == MFG_PREC_FP32 ? FMT_F16 : FMT_BF16;
     Scratch s;
+    char err[256];
     const int T = cu[n_seq];
+    const int64_t Tp = pad128(T) + 128;
     const int ldq = pad64(3 * d), ldc = pad64(d);
-    float* dq = s.alloc<float>((size_t)T * ldq);
-    CK(cudaMemcpy2D(dq, ldq * 4, qkv, 3 * d * 4, 3 * d * 4, T, cudaMemcpyHostToDevice));
+    float* dq = s.alloc<float>((size_t)T * 3 * d);
+    CK(cudaMemcpy(dq, qkv, (size_t)T * 3 * d * 4, cudaMemcpyHostToDevice));
+    auto* qh = s.alloc<uint16_t>((size_t)Tp * ldq);
+    auto* ql = split ? s.alloc<uint16_t>((size_t)Tp * ldq) : nullptr;
+    const int64_t tot = (int64_t)T * 3 * d;
+    split_rows_kernel<<<(unsigned)((tot + 255) / 256), 256>>>(dq, T, 3 * d, qh, ql, ldq, fmt);
+    CK(cudaGetLastError());
     int32_t* dcu = s.alloc<int32_t>(n_seq + 1);
     CK(cudaMemcpy(dcu, cu, (n_seq + 1) * 4, cudaMemcpyHostToDevice));
+    const bool tc_ok = use_tc && (d / n_heads == 64) && (d % 64 == 0);
     std::vector<int2> work;
-    for (int i = 0; i < n_seq; ++i)
-      for (int q = 0; q < cu[i + 1] - cu[i]; q += 64) work.push_back(make_int2(i, q));
+    std::vector<int32_t> shorts;
+    for (int i = 0; i < n_seq; ++i) {
+      const int L = cu[i + 1] - cu[i];
+      if (tc_ok && L <= 128)
+        shorts.push_back(i);
+      else
+        for (int q = 0; q < L; q += 64) work.push_back(make_int2(i, q));
+    }
     int2* dw = s.alloc<int2>(work.size());
-    CK(cudaMemcpy(dw, work.data(), work.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    if (!work.empty())
+      CK(cudaMemcpy(dw, work.data(), work.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    int32_t* dsh = s.alloc<int32_t>(shorts.size());
+    if (!shorts.empty())
+      CK(cudaMemcpy(dsh, shorts.data(), shorts.size() * 4, cudaMemcpyHostToDevice));
     auto* ch = s.alloc<uint16_t>((size_t)T * ldc);
     auto* cl = split ? s.alloc<uint16_t>((size_t)T * ldc) : nullptr;
-    CK(launch_attention(dq, ldq, d, n_heads, dcu, dw, (int)work.size(), ch, cl, ldc, fmt, nullptr, 0));
+    if (!shorts.empty()) {
+      CUtensorMap m128h, m128l, m64h, m64l;
+      if (!make_tmap_u16(&m128h, qh, Tp, ldq, ldq, 128, err, sizeof err) ||
+          !make_tmap_u16(&m64h, qh, Tp, ldq, ldq, 64, err, sizeof err))
+        throw Fail{MFG_ERR_RUNTIME, err};
+      if (split && (!make_tmap_u16(&m128l, ql, Tp, ldq, ldq, 128, err, sizeof err) ||
+                    !make_tmap_u16(&m64l, ql, Tp, ldq, ldq, 64, err, sizeof err)))
+        throw Fail{MFG_ERR_RUNTIME, err};
+      CK(launch_attention_tc(&m128h, split ? &m128l : &m128h, &m64h, split ? &m64l : &m64h, split,
+                             dcu, dsh, (int)shorts.size(), n_heads, d, fmt, ch, cl, ldc, nullptr,
+                             0));
+    }
+    if (!work.empty())
+      CK(launch_attention(qh, ql, ldq, d, n_heads, dcu, dw, (int)work.size(), ch, cl, ldc, fmt,
+                          nullptr, 0));
     float* o = s.alloc<float>((size_t)T * d);
     join_rows_kernel<<<(unsigned)(((int64_t)T * d + 255) / 256), 256>>>(ch, cl, ldc, T, d, o, fmt);
     CK(cudaGetLastError());

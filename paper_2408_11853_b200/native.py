@@ -112,7 +112,7 @@ def gpu():
             lib.mfg_reset_stats.restype = C.c_int
             lib.mfgt_gemm.argtypes = [i32, i32, i32, i32, i32, f32p, f32p, f32p, f32p, f32p]
             lib.mfgt_gemm.restype = C.c_int
-            lib.mfgt_attention.argtypes = [i32, i32, i32p, i32, i32, f32p, f32p]
+            lib.mfgt_attention.argtypes = [i32, i32, i32p, i32, i32, f32p, f32p, i32]
             lib.mfgt_attention.restype = C.c_int
             lib.mfgt_layernorm.argtypes = [i32, i32, f32p, f32p, f32p, f32p]
             lib.mfgt_layernorm.restype = C.c_int
