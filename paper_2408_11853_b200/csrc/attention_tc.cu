@@ -9,7 +9,8 @@
 //
 // Operands travel as 16-bit hi/lo pairs and each product is three MMAs
 // (hi·hi + lo·hi + hi·lo), like the GEMMs, so S and O carry ~22 significant
-// bits (fp16 pieces). Q, K, V tiles arrive by TMA (128B swizzle) straight from
+// bits (fp16 pieces). Q, K, V tiles arrive by TMA (128B swizzle, 16-row boxes so
+// only round16(L) rows are fetched) straight from
 // the QKV GEMM output; P is written by the softmax threads into the (then dead)
 // Q/K shared-memory region in the same swizzled K-major layout.
 //
@@ -32,10 +33,8 @@ __device__ __forceinline__ void tc_mma_f16kind(uint32_t d, uint64_t a, uint64_t 
 
 template <bool SPLIT>
 __global__ void __launch_bounds__(ATC_THREADS, 2)
-    attention_tc_kernel(const __grid_constant__ CUtensorMap mh128,
-                        const __grid_constant__ CUtensorMap ml128,
-                        const __grid_constant__ CUtensorMap mh64,
-                        const __grid_constant__ CUtensorMap ml64, const int32_t* __restrict__ cu,
+    attention_tc_kernel(const __grid_constant__ CUtensorMap mh,
+                        const __grid_constant__ CUtensorMap ml, const int32_t* __restrict__ cu,
                         const int32_t* __restrict__ seqs, int d, float scale, int fmt,
                         uint16_t* __restrict__ ch, uint16_t* __restrict__ cl, int ldc, int* ovf) {
   extern __shared__ uint8_t smem_raw[];
@@ -68,19 +67,19 @@ __global__ void __launch_bounds__(ATC_THREADS, 2)
   const uint32_t tm = *tslot;
 
   if (tid == 0) {
-    const bool small = L <= 64;
-    const CUtensorMap* mh = small ? &mh64 : &mh128;
-    const CUtensorMap* ml = small ? &ml64 : &ml128;
-    const uint32_t bytes = (small ? 64 : 128) * 128 * (SPLIT ? 6 : 3);
-    mbar_expect_tx(&bars[0], bytes);
+    // 16-row boxes: fetch exactly round16(L) rows of Q, K and V (hi, lo)
+    mbar_expect_tx(&bars[0], (uint32_t)n16 * 128 * (SPLIT ? 6 : 3));
     const int cq = h * 64, ck = d + h * 64, cv = 2 * d + h * 64;
-    tma_load_2d(tile + 0 * ATC_TILE, mh, &bars[0], cq, start);
-    tma_load_2d(tile + 2 * ATC_TILE, mh, &bars[0], ck, start);
-    tma_load_2d(tile + 4 * ATC_TILE, mh, &bars[0], cv, start);
-    if (SPLIT) {
-      tma_load_2d(tile + 1 * ATC_TILE, ml, &bars[0], cq, start);
-      tma_load_2d(tile + 3 * ATC_TILE, ml, &bars[0], ck, start);
-      tma_load_2d(tile + 5 * ATC_TILE, ml, &bars[0], cv, start);
+    for (int r0 = 0; r0 < n16; r0 += 16) {
+      const int so = r0 * 128;
+      tma_load_2d(tile + 0 * ATC_TILE + so, &mh, &bars[0], cq, start + r0);
+      tma_load_2d(tile + 2 * ATC_TILE + so, &mh, &bars[0], ck, start + r0);
+      tma_load_2d(tile + 4 * ATC_TILE + so, &mh, &bars[0], cv, start + r0);
+      if (SPLIT) {
+        tma_load_2d(tile + 1 * ATC_TILE + so, &ml, &bars[0], cq, start + r0);
+        tma_load_2d(tile + 3 * ATC_TILE + so, &ml, &bars[0], ck, start + r0);
+        tma_load_2d(tile + 5 * ATC_TILE + so, &ml, &bars[0], cv, start + r0);
+      }
     }
     mbar_wait(&bars[0], 0);
     tc_fence_after();
@@ -213,8 +212,7 @@ __global__ void __launch_bounds__(ATC_THREADS, 2)
   }
 }
 
-cudaError_t launch_attention_tc(const CUtensorMap* mh128, const CUtensorMap* ml128,
-                                const CUtensorMap* mh64, const CUtensorMap* ml64, bool split,
+cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml, bool split,
                                 const int32_t* cu, const int32_t* seqs, int n_seqs, int heads,
                                 int d, int fmt, uint16_t* ch, uint16_t* cl, int ldc, int* ovf,
                                 cudaStream_t st) {
@@ -224,13 +222,13 @@ cudaError_t launch_attention_tc(const CUtensorMap* mh128, const CUtensorMap* ml1
   if (split) {
     cudaFuncSetAttribute(attention_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          ATC_SMEM);
-    attention_tc_kernel<true><<<grid, ATC_THREADS, ATC_SMEM, st>>>(
-        *mh128, *ml128, *mh64, *ml64, cu, seqs, d, scale, fmt, ch, cl, ldc, ovf);
+    attention_tc_kernel<true><<<grid, ATC_THREADS, ATC_SMEM, st>>>(*mh, *ml, cu, seqs, d, scale,
+                                                                     fmt, ch, cl, ldc, ovf);
   } else {
     cudaFuncSetAttribute(attention_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          ATC_SMEM);
-    attention_tc_kernel<false><<<grid, ATC_THREADS, ATC_SMEM, st>>>(
-        *mh128, *mh128, *mh64, *mh64, cu, seqs, d, scale, fmt, ch, cl, ldc, ovf);
+    attention_tc_kernel<false><<<grid, ATC_THREADS, ATC_SMEM, st>>>(*mh, *mh, cu, seqs, d, scale,
+                                                                      fmt, ch, cl, ldc, ovf);
   }
   return cudaGetLastError();
 }

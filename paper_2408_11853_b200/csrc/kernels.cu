@@ -38,43 +38,83 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __r
 
 // ------------------------------------------------------------------ layer norm
 // out = (y - mean) / sqrt(var_pop + 1e-5) * g + b, one warp per row
-// (`encoder.py:52-57, 128-130`). Writes any of: fp32 copy, bf16 hi, bf16 lo.
-template <int VPT>
-__global__ void layernorm_kernel(const float* __restrict__ y, int T, int d, int ld,
-                                 const float* __restrict__ g, const float* __restrict__ bta,
-                                 float* __restrict__ out32, uint16_t* __restrict__ oh,
-                                 uint16_t* __restrict__ ol, int fmt, int* ovf) {
+// (`encoder.py:52-57, 128-130`). Writes any of: fp32 copy, 16-bit hi, lo pieces.
+// V4 float4 per lane (d % 4 == 0), two-pass statistics from registers.
+template <int V4>
+__global__ void __launch_bounds__(256)
+    layernorm_kernel(const float* __restrict__ y, int T, int d, int ld,
+                     const float* __restrict__ g, const float* __restrict__ bta,
+                     float* __restrict__ out32, uint16_t* __restrict__ oh,
+                     uint16_t* __restrict__ ol, int fmt, int* ovf) {
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
-  const float* row = y + (size_t)t * ld;
-  float v[VPT];
+  const float4* row = reinterpret_cast<const float4*>(y + (size_t)t * ld);
+  const int n4 = d >> 2;
+  float4 v[V4];
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
+  for (int i = 0; i < V4; ++i) {
     const int c = i * 32 + lane;
-    v[i] = (c < d) ? row[c] : 0.f;
-    s += v[i];
+    v[i] = c < n4 ? row[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
   }
   const float mean = warp_sum(s) / (float)d;
   float q = 0.f;
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int c = i * 32 + lane;
-    const float z = (c < d) ? v[i] - mean : 0.f;
-    q += z * z;
-  }
-  const float var = warp_sum(q) / (float)d;
-  const float rstd = 1.0f / sqrtf(var + 1e-5f);
-  const size_t o = (size_t)t * ld;
-#pragma unroll
-  for (int i = 0; i < VPT; ++i) {
-    const int c = i * 32 + lane;
-    if (c < d) {
-      const float r = (v[i] - mean) * rstd * g[c] + bta[c];
-      if (out32) out32[o + c] = r;
-      if (oh) store_split(oh, ol, o + c, r, fmt, ovf);
+  for (int i = 0; i < V4; ++i) {
+    if (i * 32 + lane < n4) {
+      const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, e = v[i].w - mean;
+      q += (a * a + b * b) + (c * c + e * e);
     }
+  }
+  const float rstd = 1.0f / sqrtf(warp_sum(q) / (float)d + 1e-5f);
+  const size_t o = (size_t)t * ld;
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    const int c = i * 32 + lane;
+    if (c < n4) {
+      const float4 gg = reinterpret_cast<const float4*>(g)[c];
+      const float4 bb = reinterpret_cast<const float4*>(bta)[c];
+      const float r[4] = {(v[i].x - mean) * rstd * gg.x + bb.x, (v[i].y - mean) * rstd * gg.y + bb.y,
+                          (v[i].z - mean) * rstd * gg.z + bb.z, (v[i].w - mean) * rstd * gg.w + bb.w};
+      if (out32) reinterpret_cast<float4*>(out32 + o)[c] = make_float4(r[0], r[1], r[2], r[3]);
+      if (oh) {
+        uint16_t h[4], l[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ok &= split16(r[j], fmt, h[j], l[j]);
+        reinterpret_cast<uint2*>(oh + o)[c] =
+            make_uint2(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16));
+        if (ol)
+          reinterpret_cast<uint2*>(ol + o)[c] =
+              make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
+      }
+    }
+  }
+  if (!ok && ovf) atomicOr(ovf, 1);
+}
+
+// Scalar fallback for d % 4 != 0.
+__global__ void layernorm_scalar_kernel(const float* __restrict__ y, int T, int d, int ld,
+                                        const float* __restrict__ g, const float* __restrict__ bta,
+                                        float* __restrict__ out32, uint16_t* __restrict__ oh,
+                                        uint16_t* __restrict__ ol, int fmt, int* ovf) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const float* row = y + (size_t)t * ld;
+  float s = 0.f;
+  for (int c = lane; c < d; c += 32) s += row[c];
+  const float mean = warp_sum(s) / (float)d;
+  float q = 0.f;
+  for (int c = lane; c < d; c += 32) q += (row[c] - mean) * (row[c] - mean);
+  const float rstd = 1.0f / sqrtf(warp_sum(q) / (float)d + 1e-5f);
+  const size_t o = (size_t)t * ld;
+  for (int c = lane; c < d; c += 32) {
+    const float r = (row[c] - mean) * rstd * g[c] + bta[c];
+    if (out32) out32[o + c] = r;
+    if (oh) store_split(oh, ol, o + c, r, fmt, ovf);
   }
 }
 
@@ -329,17 +369,22 @@ cudaError_t launch_layernorm(const float* y, int T, int d, int ld, const float* 
                              float* out32, uint16_t* oh, uint16_t* ol, int fmt, int* ovf,
                              cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  const int vpt = (d + 31) / 32;
   dim3 grid((T + 7) / 8), block(256);
+  const bool vec = d % 4 == 0 && ld % 4 == 0 && ((uintptr_t)y & 15) == 0 &&
+                   ((uintptr_t)g & 15) == 0 && ((uintptr_t)b & 15) == 0;
+  const int v4 = (d / 4 + 31) / 32;
+  if (vec) {
 #define LN_CASE(V)                                                                   \
-  if (vpt <= V) {                                                                    \
-    layernorm_kernel<V><<<grid, block, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol, fmt, ovf);   \
-    return cudaGetLastError();                                                       \
-  }
-  LN_CASE(1) LN_CASE(2) LN_CASE(4) LN_CASE(8) LN_CASE(16) LN_CASE(24) LN_CASE(32)
-  LN_CASE(36) LN_CASE(40) LN_CASE(48) LN_CASE(64) LN_CASE(80) LN_CASE(96) LN_CASE(128)
+    if (v4 <= V) {                                                                   \
+      layernorm_kernel<V><<<grid, block, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol, fmt, ovf); \
+      return cudaGetLastError();                                                     \
+    }
+    LN_CASE(1) LN_CASE(2) LN_CASE(4) LN_CASE(8) LN_CASE(9) LN_CASE(10) LN_CASE(12) LN_CASE(16)
+    LN_CASE(20) LN_CASE(24) LN_CASE(32)
 #undef LN_CASE
-  return cudaErrorInvalidValue;
+  }
+  layernorm_scalar_kernel<<<grid, block, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol, fmt, ovf);
+  return cudaGetLastError();
 }
 
 template <int DHC>

@@ -20,9 +20,8 @@ cudaError_t launch_attention(const uint16_t* qh, const uint16_t* ql, int ldq, in
                              const int2* work, int n_work, uint16_t* ch, uint16_t* cl,
                              int ldc, int fmt, int* ovf, cudaStream_t st);
 // tcgen05 attention, one CTA per (listed sequence, head); L <= 128, d_head == 64.
-// Maps: Q|K|V hi/lo [T][ldq] with box {64 cols, 128 rows} and {64, 64}.
-cudaError_t launch_attention_tc(const CUtensorMap* mh128, const CUtensorMap* ml128,
-                                const CUtensorMap* mh64, const CUtensorMap* ml64, bool split,
+// Maps: Q|K|V hi/lo [T][ldq] with box {64 cols, 16 rows}.
+cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml, bool split,
                                 const int32_t* cu, const int32_t* seqs, int n_seqs, int heads,
                                 int d, int fmt, uint16_t* ch, uint16_t* cl, int ldc, int* ovf,
                                 cudaStream_t st);

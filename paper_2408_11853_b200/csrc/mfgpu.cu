@@ -93,7 +93,7 @@ struct mfg_ctx {
   int cap_records = 0;
   float *x32 = nullptr, *y32 = nullptr;
   Act xa, ca, ha, fa, qa;          // qa: Q|K|V pieces [T][qkv_ld]
-  CUtensorMap qmh64{}, qml64{};     // Q|K|V maps with 64-row boxes (short sequences)
+  CUtensorMap qmh16{}, qml16{};     // Q|K|V maps with 16-row boxes (attention)
   bool att_tc = false;              // tcgen05 attention usable (d_head == 64)
   int32_t *d_short = nullptr, *h_short = nullptr;
   std::vector<Act> ga;  // head hidden-stage outputs
@@ -326,9 +326,9 @@ struct mfg_ctx {
     make_act(qa, cap_tokens, qkv_ld);
     {
       char err[256];
-      if (!make_tmap_u16(&qmh64, qa.hi, qa.rows, qa.ld, qa.ld, 64, err, sizeof err))
+      if (!make_tmap_u16(&qmh16, qa.hi, qa.rows, qa.ld, qa.ld, 16, err, sizeof err))
         throw Fail{MFG_ERR_RUNTIME, err};
-      if (split && !make_tmap_u16(&qml64, qa.lo, qa.rows, qa.ld, qa.ld, 64, err, sizeof err))
+      if (split && !make_tmap_u16(&qml16, qa.lo, qa.rows, qa.ld, qa.ld, 16, err, sizeof err))
         throw Fail{MFG_ERR_RUNTIME, err};
     }
     att_tc = (d / H == 64) && (d % 64 == 0);
@@ -414,9 +414,8 @@ struct mfg_ctx {
         const double bytes = (double)T * d * 4 * (split ? 4 : 2);
         int e = ev_begin();
         if (n_short > 0)
-          CK(launch_attention_tc(&qa.mh, split ? &qa.ml : &qa.mh, &qmh64, split ? &qml64 : &qmh64,
-                                 split, d_cu, d_short, n_short, H, d, fmt, ca.hi, ca.lo, ca.ld,
-                                 d_ovf, st));
+          CK(launch_attention_tc(&qmh16, split ? &qml16 : &qmh16, split, d_cu, d_short, n_short,
+                                 H, d, fmt, ca.hi, ca.lo, ca.ld, d_ovf, st));
         if (n_work > 0)
           CK(launch_attention(qa.hi, qa.lo, qa.ld, d, H, d_cu, d_work, (int)n_work, ca.hi, ca.lo,
                               ca.ld, fmt, d_ovf, st));
@@ -875,16 +874,13 @@ extern "C" int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* c
     auto* ch = s.alloc<uint16_t>((size_t)T * ldc);
     auto* cl = split ? s.alloc<uint16_t>((size_t)T * ldc) : nullptr;
     if (!shorts.empty()) {
-      CUtensorMap m128h, m128l, m64h, m64l;
-      if (!make_tmap_u16(&m128h, qh, Tp, ldq, ldq, 128, err, sizeof err) ||
-          !make_tmap_u16(&m64h, qh, Tp, ldq, ldq, 64, err, sizeof err))
+      CUtensorMap m16h, m16l;
+      if (!make_tmap_u16(&m16h, qh, Tp, ldq, ldq, 16, err, sizeof err))
         throw Fail{MFG_ERR_RUNTIME, err};
-      if (split && (!make_tmap_u16(&m128l, ql, Tp, ldq, ldq, 128, err, sizeof err) ||
-                    !make_tmap_u16(&m64l, ql, Tp, ldq, ldq, 64, err, sizeof err)))
+      if (split && !make_tmap_u16(&m16l, ql, Tp, ldq, ldq, 16, err, sizeof err))
         throw Fail{MFG_ERR_RUNTIME, err};
-      CK(launch_attention_tc(&m128h, split ? &m128l : &m128h, &m64h, split ? &m64l : &m64h, split,
-                             dcu, dsh, (int)shorts.size(), n_heads, d, fmt, ch, cl, ldc, nullptr,
-                             0));
+      CK(launch_attention_tc(&m16h, split ? &m16l : &m16h, split, dcu, dsh, (int)shorts.size(),
+                             n_heads, d, fmt, ch, cl, ldc, nullptr, 0));
     }
     if (!work.empty())
       CK(launch_attention(qh, ql, ldq, d, n_heads, dcu, dw, (int)work.size(), ch, cl, ldc, fmt,

@@ -1,0 +1,148 @@
+"""Segment-level data parallelism across the GPUs of one box.
+
+The reference's only parallelism is a thread pool mapping `score_records`
+over the mini-batches of a window (`pkg/src/metricforge/evaluate.py:154-158,
+171-175`); results are bitwise independent of the worker count
+(`tests/test_evaluate.py:92-98`). Here the workers are processes, one per GPU
+(`torchrun`, RANK / WORLD_SIZE / LOCAL_RANK):
+
+  * every rank tokenises the same input and computes the same global plan
+    (windows -> bit-exact length sort -> mini-batches);
+  * mini-batches are assigned to ranks longest-processing-time-first on the
+    cost  sum_seq (L * c_gemm + L^2 * c_attn)  (round-robin per window would
+    always give the longest, sorted-first batch to rank 0);
+  * each rank scores its batches in one device call per window, the
+    (plan position, score) pairs are all-gathered, and the plan's inverse
+    permutation restores input order.
+
+There is no collective on the data path: records are independent, the only
+exchange is the final gather of float32 scores. Scores are bitwise identical
+at any world size because no kernel's reduction order depends on batch
+composition.
+"""
+
+from __future__ import annotations
+
+import heapq
+import math
+import os
+from typing import Callable, Optional
+
+import numpy as np
+
+from .batching import BatchConfig, pack_roles, plan_order
+from .evaluate import ScoreReport, records_from_tsv_lines
+from .kinds import N_SEQUENCES, Kind
+
+# relative per-token GEMM cost vs per-token-pair attention cost (config-2 scale:
+# 2*(4d^2 + 2 d f) per token, 4 d per token pair)
+C_GEMM = 2.0 * (4 * 1024 ** 2 + 2 * 1024 * 4096)
+C_ATTN = 4.0 * 1024
+
+
+def batch_cost(seq_lens) -> float:
+    L = np.asarray(seq_lens, dtype=np.float64)
+    return float((L * C_GEMM + L * L * C_ATTN).sum())
+
+
+def lpt_assign(costs, world: int):
+    """Longest-processing-time-first: returns one list of batch indices per rank.
+    Deterministic (ties broken by batch index, then rank)."""
+    order = sorted(range(len(costs)), key=lambda i: (-costs[i], i))
+    heap = [(0.0, r) for r in range(world)]
+    out = [[] for _ in range(world)]
+    for i in order:
+        load, r = heapq.heappop(heap)
+        out[r].append(i)
+        heapq.heappush(heap, (load + costs[i], r))
+    return [sorted(b) for b in out]
+
+
+def shard_plan(seq_off, n_seq, n_records, config: BatchConfig, world: int):
+    """Global plan of a record-major encoding and its LPT assignment.
+
+    Returns (order, batches, assignment): order[pos] = record index; batches =
+    list of (start, stop) plan-position ranges (one mini-batch each); assignment
+    = per rank list of batch indices."""
+    lens = np.diff(seq_off).reshape(n_records, n_seq)
+    order = plan_order(lens.sum(axis=1), config)
+    mb = config.mini_batch
+    batches = [(s, min(n_records, s + mb)) for s in range(0, n_records, mb)]
+    costs = [batch_cost(lens[order[a:b]].ravel()) for a, b in batches]
+    return order, batches, lpt_assign(costs, world)
+
+
+def score_sharded(model_score: Callable, vocab, kind, field_texts, max_len, config: BatchConfig,
+                  rank: int, world: int, gather: Optional[Callable] = None, n_threads: int = 0):
+    """Score `field_texts` (per-record field lists) across `world` ranks.
+
+    model_score(ids, cu, n) -> float32[n] scores role-major packed records (e.g.
+    GpuScoringModel.score_packed); gather(obj) -> list of obj from all ranks
+    (e.g. torch.distributed.all_gather_object). Returns scores in input order
+    (on every rank)."""
+    kind = Kind.parse(kind)
+    n = len(field_texts)
+    ns = N_SEQUENCES[kind]
+    ids, seq_off = vocab.encode_batch(kind, field_texts, max_len, n_threads)
+    order, batches, assign = shard_plan(seq_off, ns, n, config, world)
+    mine = assign[rank]
+    pos = np.concatenate([np.arange(*batches[b]) for b in mine]) if mine else np.zeros(0, np.int64)
+    if len(pos):
+        packed, cu = pack_roles(ids, seq_off, ns, order[pos])
+        scores = np.asarray(model_score(packed, cu, len(pos)), dtype=np.float32)
+    else:
+        scores = np.zeros(0, np.float32)
+    parts = gather((pos, scores)) if gather is not None else [(pos, scores)]
+    flat = np.empty(n, dtype=np.float32)
+    seen = 0
+    for p, s in parts:
+        flat[order[p]] = s
+        seen += len(p)
+    if seen != n:
+        raise RuntimeError(f"gathered {seen} scores for {n} records")
+    return flat
+
+
+class DistributedEvaluator:
+    """`Evaluator` over all ranks of an initialised torch.distributed group.
+
+    Every rank passes the same lines; every rank gets the full report."""
+
+    def __init__(self, config, group=None):
+        import torch.distributed as dist
+
+        from .evaluate import Evaluator
+
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if config.device is None:
+            config.device = int(os.environ.get("LOCAL_RANK", "0"))
+        self.ev = Evaluator(config)
+        self.config = config
+        self._group = group
+
+    def _gather(self, obj):
+        import torch.distributed as dist
+
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        dist.all_gather_object(out, obj, group=self._group)
+        return out
+
+    def evaluate_lines(self, lines) -> ScoreReport:
+        kind = self.ev.kind
+        recs = [r.field_values(kind, i) for i, r in enumerate(records_from_tsv_lines(lines, kind))]
+        scores = score_sharded(self.ev.model.score_packed, self.ev.vocab, kind, recs,
+                               self.ev.max_len, self.config.batch, self.rank, self.world,
+                               self._gather, self.config.tokenizer_threads)
+        return ScoreReport(segment_scores=scores.tolist())
+
+    def close(self):
+        self.ev.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
