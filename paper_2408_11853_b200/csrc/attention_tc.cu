@@ -1,212 +1,277 @@
-// tcgen05 attention for one (sequence, head) per CTA, sequences of <= 128
-// tokens with d_head == 64 (XLM-R / InfoXLM / RemBERT shapes; the path of
-// `pkg/src/metricforge/encoder.py:132-147` for every record of configs 2-4).
+// Persistent tcgen05 attention for sequences of <= 128 tokens with d_head 64
+// (XLM-R / InfoXLM / RemBERT shapes: every record of configs 2-4). Replaces the
+// per-head loop of `pkg/src/metricforge/encoder.py:132-147` (+ masked_softmax 60-66).
 //
-//   S = Q·Kᵀ      tcgen05.mma M=128 x N=round16(L) x K=64, fp32 in TMEM
-//   P = exp(S·scale - rowmax)  (fp32, exact expf, keys >= L get exactly 0)
-//   O = P·V       tcgen05.mma M=128 x N=64 x K=round16(L), V read MN-major
-//   ctx = O / rowsum  -> 16-bit hi/lo pieces (the O-projection's A operand)
+// Work item = (sequence, head). Per item:
+//   S = Q·Kᵀ      tcgen05.mma M=128 x N=round16(L) x K=64 -> fp32 in TMEM
+//   P = exp(S·scale - rowmax) = exp2f((S - rowmax)·scale·log2e) in fp32, keys >= L
+//       get exactly 0
+//   O = P·V       tcgen05.mma M=128 x N=64 x K=round16(L), V is an MN-major B
+//   ctx = O / rowsum -> 16-bit hi/lo pieces (the O-projection's A operand)
+// Operands are 16-bit hi/lo pairs and each product is three MMAs
+// (hi·hi + lo·hi + hi·lo), like the GEMMs (~22 significant bits with fp16).
 //
-// Operands travel as 16-bit hi/lo pairs and each product is three MMAs
-// (hi·hi + lo·hi + hi·lo), like the GEMMs, so S and O carry ~22 significant
-// bits (fp16 pieces). Q, K, V tiles arrive by TMA (128B swizzle, 16-row boxes so
-// only round16(L) rows are fetched) straight from
-// the QKV GEMM output; P is written by the softmax threads into the (then dead)
-// Q/K shared-memory region in the same swizzled K-major layout.
-//
-// 128 threads: thread r owns query row r (TMEM lane r). Thread 0 issues TMA and
-// MMAs; warp 0 owns the TMEM allocation (256 columns: S 0..127, O 128..191).
-// ~97 KB shared memory -> two CTAs per SM overlap softmax with MMA/TMA.
+// One CTA per SM walks items round-robin. Items alternate between two lanes
+// b = k & 1, each with its own smem buffer, TMEM region (S, then O in the same
+// columns once S is dead) and softmax warp group, so one group's softmax runs
+// while the other waits for its P·V MMAs and the TMA/MMA of later items:
+//   warp 0 lane 0  TMA producer  (Q, K, V tiles, 16-row boxes, 128B swizzle)
+//   warp 1 lane 0  MMA issuer    (S(k), S(k+1), then O(k) as soon as P(k) lands)
+//   warps 2-5 / 6-9  softmax (row = TMEM lane, two TMEM passes: max, exp) and
+//                  epilogue for the items of lane 0 / lane 1
+// P is written, swizzled K-major, into the item's (dead) Q/K smem tiles.
 #include "kernels.h"
 #include "ptx.cuh"
 
 namespace mfg {
 
-constexpr int ATC_THREADS = 128;
-constexpr int ATC_TILE = 128 * 128;  // bytes of one 128-row x 64-col 16-bit tile
-constexpr int ATC_SMEM = 1024 + 6 * ATC_TILE + 64;
+constexpr int ATP_THREADS = 320;
+constexpr int ATP_TILE = 128 * 128;            // one 128-row x 64-col 16-bit tile
+constexpr int ATP_BUF = 6 * ATP_TILE;          // Qh Ql Kh Kl Vh Vl
+constexpr int ATP_SMEM = 1024 + 2 * ATP_BUF + 256;
 
-__device__ __forceinline__ void tc_mma_f16kind(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                               uint32_t acc) {
-  tc_mma_bf16(d, a, b, idesc, acc);
+struct AttItem {
+  int start, L, h;
+};
+
+__device__ __forceinline__ AttItem att_item(int it, const int32_t* cu, const int32_t* seqs,
+                                            int heads) {
+  const int s = seqs[it / heads];
+  AttItem a;
+  a.start = cu[s];
+  a.L = cu[s + 1] - a.start;
+  a.h = it % heads;
+  return a;
 }
 
 template <bool SPLIT>
-__global__ void __launch_bounds__(ATC_THREADS, 2)
+__global__ void __launch_bounds__(ATP_THREADS, 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap mh,
                         const __grid_constant__ CUtensorMap ml, const int32_t* __restrict__ cu,
-                        const int32_t* __restrict__ seqs, int d, float scale, int fmt,
-                        uint16_t* __restrict__ ch, uint16_t* __restrict__ cl, int ldc, int* ovf) {
+                        const int32_t* __restrict__ seqs, int n_items, int heads, int d,
+                        float scale, int fmt, uint16_t* __restrict__ ch,
+                        uint16_t* __restrict__ cl, int ldc, int* ovf) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
-  // tiles: 0 Qh, 1 Ql, 2 Kh, 3 Kl, 4 Vh, 5 Vl; after S: P_hi = tiles 0,1 (keys 0-63,
-  // 64-127), P_lo = tiles 2,3.
-  uint8_t* tile = sm;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 6 * ATC_TILE);  // load, s, o
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 2 * ATP_BUF);
+  uint64_t* load_full = bars;       // [2]
+  uint64_t* s_full = bars + 2;      // [2]
+  uint64_t* p_full = bars + 4;      // [2]
+  uint64_t* o_full = bars + 6;      // [2]  also: smem buffer free again
+  uint64_t* t_empty = bars + 8;     // [2]  TMEM (S, O) buffer free again
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 10);
 
-  const int seq = seqs[blockIdx.x];
-  const int h = blockIdx.y;
-  const int start = cu[seq];
-  const int L = cu[seq + 1] - start;
-  const int n16 = (L + 15) & ~15;
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_init(&bars[2], 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&load_full[b], 1);
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 4);
+      mbar_init(&o_full[b], 1);
+      mbar_init(&t_empty[b], 4);
+    }
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<256>(tslot);
+  if (warp == 1) tmem_alloc<256>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tm = *tslot;
+  auto buf = [&](int b) { return sm + b * ATP_BUF; };
 
-  if (tid == 0) {
-    // 16-row boxes: fetch exactly round16(L) rows of Q, K and V (hi, lo)
-    mbar_expect_tx(&bars[0], (uint32_t)n16 * 128 * (SPLIT ? 6 : 3));
-    const int cq = h * 64, ck = d + h * 64, cv = 2 * d + h * 64;
-    for (int r0 = 0; r0 < n16; r0 += 16) {
-      const int so = r0 * 128;
-      tma_load_2d(tile + 0 * ATC_TILE + so, &mh, &bars[0], cq, start + r0);
-      tma_load_2d(tile + 2 * ATC_TILE + so, &mh, &bars[0], ck, start + r0);
-      tma_load_2d(tile + 4 * ATC_TILE + so, &mh, &bars[0], cv, start + r0);
-      if (SPLIT) {
-        tma_load_2d(tile + 1 * ATC_TILE + so, &ml, &bars[0], cq, start + r0);
-        tma_load_2d(tile + 3 * ATC_TILE + so, &ml, &bars[0], ck, start + r0);
-        tma_load_2d(tile + 5 * ATC_TILE + so, &ml, &bars[0], cv, start + r0);
-      }
-    }
-    mbar_wait(&bars[0], 0);
-    tc_fence_after();
-    // S[128 x n16] = Q Kᵀ
-    const uint32_t idesc = idesc_f16kind(128, n16, fmt);
-    const uint64_t qh = umma_desc_sw128(tile), kh = umma_desc_sw128(tile + 2 * ATC_TILE);
-    const uint64_t ql = umma_desc_sw128(tile + ATC_TILE), kl = umma_desc_sw128(tile + 3 * ATC_TILE);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint64_t adv = (uint64_t)(k * 32) >> 4;
-      tc_mma_f16kind(tm, qh + adv, kh + adv, idesc, k != 0);
-      if (SPLIT) {
-        tc_mma_f16kind(tm, ql + adv, kh + adv, idesc, 1);
-        tc_mma_f16kind(tm, qh + adv, kl + adv, idesc, 1);
-      }
-    }
-    tc_commit(&bars[1]);
-  }
-  __syncwarp();
-
-  // ---- softmax: thread tid owns query row tid
-  mbar_wait(&bars[1], 0);
-  tc_fence_after();
-  const uint32_t trow = tm + ((uint32_t)(warp * 32) << 16);
-  const int nchunk = (L + 31) >> 5;
-  float mx = -INFINITY;
-  for (int c = 0; c < nchunk; ++c) {
-    float v[32];
-    tmem_ld_32x32(trow + c * 32, v);
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (c * 32 + i < L) mx = fmaxf(mx, v[i] * scale);
-  }
-  float sum = 0.f;
-  const int r = tid;
-  for (int c = 0; c < nchunk; ++c) {
-    float v[32];
-    tmem_ld_32x32(trow + c * 32, v);
-    uint32_t ph[16], pl[16];
-#pragma unroll
-    for (int i = 0; i < 32; i += 2) {
-      float p0 = 0.f, p1 = 0.f;
-      if (c * 32 + i < L) p0 = expf(v[i] * scale - mx);
-      if (c * 32 + i + 1 < L) p1 = expf(v[i + 1] * scale - mx);
-      sum += p0 + p1;
-      uint16_t h0, l0, h1, l1;
-      split16(p0, fmt, h0, l0);
-      split16(p1, fmt, h1, l1);
-      ph[i / 2] = h0 | ((uint32_t)h1 << 16);
-      pl[i / 2] = l0 | ((uint32_t)l1 << 16);
-    }
-    // keys c*32..c*32+31 -> atom c/2, 16-byte units (c%2)*4 .. +3, swizzled by row
-    uint8_t* hi_atom = tile + (c >> 1) * ATC_TILE;
-    uint8_t* lo_atom = tile + (2 + (c >> 1)) * ATC_TILE;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int unit = (c & 1) * 4 + u;
-      const uint32_t off = r * 128 + ((unit ^ (r & 7)) << 4);
-      *reinterpret_cast<uint4*>(hi_atom + off) =
-          make_uint4(ph[4 * u], ph[4 * u + 1], ph[4 * u + 2], ph[4 * u + 3]);
-      if (SPLIT)
-        *reinterpret_cast<uint4*>(lo_atom + off) =
-            make_uint4(pl[4 * u], pl[4 * u + 1], pl[4 * u + 2], pl[4 * u + 3]);
-    }
-  }
-  // P (generic-proxy smem writes) must be visible to the tensor core (async proxy)
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-
-  if (tid == 0) {
-    // O[128 x 64] = P V, V is [keys][64] = MN-major B operand
-    const uint32_t idesc = idesc_f16kind(128, 64, fmt) | (1u << 16);
-    const uint32_t to = tm + 128;
-    for (int k = 0; k < n16; k += 16) {
-      const int atom = k >> 6;
-      const uint64_t aoff = (uint64_t)((k & 63) * 2) >> 4;
-      const uint64_t ph_ = umma_desc_sw128(tile + atom * ATC_TILE) + aoff;
-      const uint64_t pl_ = umma_desc_sw128(tile + (2 + atom) * ATC_TILE) + aoff;
-      const uint64_t vh = umma_desc_sw128(tile + 4 * ATC_TILE + k * 128);
-      const uint64_t vl = umma_desc_sw128(tile + 5 * ATC_TILE + k * 128);
-      tc_mma_f16kind(to, ph_, vh, idesc, k != 0);
-      if (SPLIT) {
-        tc_mma_f16kind(to, pl_, vh, idesc, 1);
-        tc_mma_f16kind(to, ph_, vl, idesc, 1);
-      }
-    }
-    tc_commit(&bars[2]);
-  }
-  __syncwarp();
-  mbar_wait(&bars[2], 0);
-  tc_fence_after();
-  {
-    // every lane runs the (warp-collective) TMEM loads; only rows < L store
-    const float inv = 1.0f / sum;
-    const size_t ob = (size_t)(start + r) * ldc + h * 64;
-    bool ok = true;
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      float v[32];
-      tmem_ld_32x32(trow + 128 + c * 32, v);
-      if (r < L) {
-        uint32_t hh[16], ll[16];
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          uint16_t h0, l0, h1, l1;
-          ok &= split16(v[i] * inv, fmt, h0, l0);
-          ok &= split16(v[i + 1] * inv, fmt, h1, l1);
-          hh[i / 2] = h0 | ((uint32_t)h1 << 16);
-          ll[i / 2] = l0 | ((uint32_t)l1 << 16);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          *reinterpret_cast<uint4*>(ch + ob + c * 32 + 8 * u) =
-              make_uint4(hh[4 * u], hh[4 * u + 1], hh[4 * u + 2], hh[4 * u + 3]);
-          if (SPLIT)
-            *reinterpret_cast<uint4*>(cl + ob + c * 32 + 8 * u) =
-                make_uint4(ll[4 * u], ll[4 * u + 1], ll[4 * u + 2], ll[4 * u + 3]);
-        }
-      }
-    }
-    if (!ok && ovf) atomicOr(ovf, 1);
-  }
-  tc_fence_before();
-  __syncthreads();
   if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int k = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++k) {
+        const int b = k & 1;
+        const uint32_t ph = (k >> 1) & 1;
+        const AttItem a = att_item(it, cu, seqs, heads);
+        const int n16 = (a.L + 15) & ~15;
+        mbar_wait(&o_full[b], ph ^ 1);  // item k-2 finished reading this buffer
+        mbar_expect_tx(&load_full[b], (uint32_t)n16 * 128 * (SPLIT ? 6 : 3));
+        const int cq = a.h * 64, ck = d + a.h * 64, cv = 2 * d + a.h * 64;
+        uint8_t* t = buf(b);
+        for (int r0 = 0; r0 < n16; r0 += 16) {
+          const int so = r0 * 128;
+          tma_load_2d(t + 0 * ATP_TILE + so, &mh, &load_full[b], cq, a.start + r0);
+          tma_load_2d(t + 2 * ATP_TILE + so, &mh, &load_full[b], ck, a.start + r0);
+          tma_load_2d(t + 4 * ATP_TILE + so, &mh, &load_full[b], cv, a.start + r0);
+          if (SPLIT) {
+            tma_load_2d(t + 1 * ATP_TILE + so, &ml, &load_full[b], cq, a.start + r0);
+            tma_load_2d(t + 3 * ATP_TILE + so, &ml, &load_full[b], ck, a.start + r0);
+            tma_load_2d(t + 5 * ATP_TILE + so, &ml, &load_full[b], cv, a.start + r0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      auto issue_s = [&](int it, int k) {
+        const int b = k & 1;
+        const uint32_t ph = (k >> 1) & 1;
+        const AttItem a = att_item(it, cu, seqs, heads);
+        const int n16 = (a.L + 15) & ~15;
+        mbar_wait(&t_empty[b], ph ^ 1);   // epilogue of item k-2 read its O
+        mbar_wait(&load_full[b], ph);
+        tc_fence_after();
+        const uint32_t idesc = idesc_f16kind(128, n16, fmt);
+        uint8_t* t = buf(b);
+        const uint64_t qh = umma_desc_sw128(t), kh = umma_desc_sw128(t + 2 * ATP_TILE);
+        const uint64_t ql = umma_desc_sw128(t + ATP_TILE), kl = umma_desc_sw128(t + 3 * ATP_TILE);
+        const uint32_t ts = tm + b * 128;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t adv = (uint64_t)(kk * 32) >> 4;
+          tc_mma_bf16(ts, qh + adv, kh + adv, idesc, kk != 0);
+          if (SPLIT) {
+            tc_mma_bf16(ts, ql + adv, kh + adv, idesc, 1);
+            tc_mma_bf16(ts, qh + adv, kl + adv, idesc, 1);
+          }
+        }
+        tc_commit(&s_full[b]);
+      };
+      int k = 0;
+      int it = blockIdx.x;
+      if (it < n_items) issue_s(it, 0);
+      if (it + (int)gridDim.x < n_items) issue_s(it + gridDim.x, 1);
+      for (; it < n_items; it += gridDim.x, ++k) {
+        const int b = k & 1;
+        const uint32_t ph = (k >> 1) & 1;
+        const AttItem a = att_item(it, cu, seqs, heads);
+        const int n16 = (a.L + 15) & ~15;
+        mbar_wait(&p_full[b], ph);
+        tc_fence_after();
+        const uint32_t idesc = idesc_f16kind(128, 64, fmt) | (1u << 16);  // B MN-major
+        uint8_t* t = buf(b);
+        const uint32_t to = tm + b * 128;  // S is dead once P(k) landed
+        for (int kk = 0; kk < n16; kk += 16) {
+          const int atom = kk >> 6;
+          const uint64_t aoff = (uint64_t)((kk & 63) * 2) >> 4;
+          const uint64_t ph_ = umma_desc_sw128(t + atom * ATP_TILE) + aoff;
+          const uint64_t pl_ = umma_desc_sw128(t + (2 + atom) * ATP_TILE) + aoff;
+          const uint64_t vh = umma_desc_sw128(t + 4 * ATP_TILE + kk * 128);
+          const uint64_t vl = umma_desc_sw128(t + 5 * ATP_TILE + kk * 128);
+          tc_mma_bf16(to, ph_, vh, idesc, kk != 0);
+          if (SPLIT) {
+            tc_mma_bf16(to, pl_, vh, idesc, 1);
+            tc_mma_bf16(to, ph_, vl, idesc, 1);
+          }
+        }
+        tc_commit(&o_full[b]);
+        const int nxt2 = it + 2 * gridDim.x;
+        if (nxt2 < n_items) issue_s(nxt2, k + 2);  // waits for epilogue(k) to free region b
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax + epilogue
+    const int g = (warp - 2) >> 2;   // lane (buffer) this group serves: items k = g, g+2, ...
+    const int q = warp & 3;          // TMEM lane quarter
+    const int r = q * 32 + lane;     // query row owned by this thread
+    const float c2 = scale * 1.4426950408889634f;  // exp(x*scale) = 2^(x*c2)
+    int j = 0;
+    for (int it = blockIdx.x + g * gridDim.x; it < n_items; it += 2 * gridDim.x, ++j) {
+      const int b = g;
+      const uint32_t ph = j & 1;
+      const AttItem a = att_item(it, cu, seqs, heads);
+      const bool active = q * 32 < a.L;  // warp-uniform: warp owns >= 1 real row
+      const uint32_t trow = tm + b * 128 + ((uint32_t)(q * 32) << 16);
+      // ---- softmax: S row -> registers (single TMEM pass) -> P pieces in smem
+      mbar_wait(&s_full[b], ph);
+      tc_fence_after();
+      float sum = 1.f;
+      if (active) {
+        // two TMEM passes (max, then exp) keep the row out of registers
+        const int nchunk = (a.L + 31) >> 5;
+        float mx = -INFINITY;
+        for (int c = 0; c < nchunk; ++c) {
+          float v[32];
+          tmem_ld_32x32(trow + c * 32, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i < a.L) mx = fmaxf(mx, v[i]);
+        }
+        sum = 0.f;
+        uint8_t* t = buf(b);
+        for (int c = 0; c < nchunk; ++c) {
+          float v[32];
+          tmem_ld_32x32(trow + c * 32, v);
+          uint32_t hh[16], ll[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float p0 = 0.f, p1 = 0.f;
+            if (c * 32 + i < a.L) p0 = exp2f((v[i] - mx) * c2);
+            if (c * 32 + i + 1 < a.L) p1 = exp2f((v[i + 1] - mx) * c2);
+            sum += p0 + p1;
+            uint16_t h0, l0, h1, l1;
+            split16(p0, fmt, h0, l0);
+            split16(p1, fmt, h1, l1);
+            hh[i / 2] = h0 | ((uint32_t)h1 << 16);
+            ll[i / 2] = l0 | ((uint32_t)l1 << 16);
+          }
+          uint8_t* hi_atom = t + (c >> 1) * ATP_TILE;
+          uint8_t* lo_atom = t + (2 + (c >> 1)) * ATP_TILE;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int unit = (c & 1) * 4 + u;
+            const uint32_t off = r * 128 + ((unit ^ (r & 7)) << 4);
+            *reinterpret_cast<uint4*>(hi_atom + off) =
+                make_uint4(hh[4 * u], hh[4 * u + 1], hh[4 * u + 2], hh[4 * u + 3]);
+            if (SPLIT)
+              *reinterpret_cast<uint4*>(lo_atom + off) =
+                  make_uint4(ll[4 * u], ll[4 * u + 1], ll[4 * u + 2], ll[4 * u + 3]);
+          }
+        }
+        // generic-proxy smem writes of P -> visible to the tensor core
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b]);
+      // ---- epilogue: O row / rowsum -> ctx pieces
+      mbar_wait(&o_full[b], ph);
+      tc_fence_after();
+      if (active) {
+        const float inv = 1.0f / sum;
+        const size_t ob = (size_t)(a.start + r) * ldc + a.h * 64;
+        bool ok = true;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          float v[32];
+          tmem_ld_32x32(trow + c * 32, v);
+          if (r < a.L) {
+            uint32_t hh[16], ll[16];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              uint16_t h0, l0, h1, l1;
+              ok &= split16(v[i] * inv, fmt, h0, l0);
+              ok &= split16(v[i + 1] * inv, fmt, h1, l1);
+              hh[i / 2] = h0 | ((uint32_t)h1 << 16);
+              ll[i / 2] = l0 | ((uint32_t)l1 << 16);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              *reinterpret_cast<uint4*>(ch + ob + c * 32 + 8 * u) =
+                  make_uint4(hh[4 * u], hh[4 * u + 1], hh[4 * u + 2], hh[4 * u + 3]);
+              if (SPLIT)
+                *reinterpret_cast<uint4*>(cl + ob + c * 32 + 8 * u) =
+                    make_uint4(ll[4 * u], ll[4 * u + 1], ll[4 * u + 2], ll[4 * u + 3]);
+            }
+          }
+        }
+        if (!ok && ovf) atomicOr(ovf, 1);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&t_empty[b]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<256>(tm);
   }
@@ -215,20 +280,21 @@ __global__ void __launch_bounds__(ATC_THREADS, 2)
 cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml, bool split,
                                 const int32_t* cu, const int32_t* seqs, int n_seqs, int heads,
                                 int d, int fmt, uint16_t* ch, uint16_t* cl, int ldc, int* ovf,
-                                cudaStream_t st) {
+                                int num_sms, cudaStream_t st) {
   if (n_seqs <= 0) return cudaSuccess;
   const float scale = 1.0f / sqrtf((float)d / (float)heads);
-  dim3 grid(n_seqs, heads);
+  const int n_items = n_seqs * heads;
+  const int grid = n_items < num_sms ? n_items : num_sms;
   if (split) {
     cudaFuncSetAttribute(attention_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         ATC_SMEM);
-    attention_tc_kernel<true><<<grid, ATC_THREADS, ATC_SMEM, st>>>(*mh, *ml, cu, seqs, d, scale,
-                                                                     fmt, ch, cl, ldc, ovf);
+                         ATP_SMEM);
+    attention_tc_kernel<true><<<grid, ATP_THREADS, ATP_SMEM, st>>>(
+        *mh, *ml, cu, seqs, n_items, heads, d, scale, fmt, ch, cl, ldc, ovf);
   } else {
     cudaFuncSetAttribute(attention_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         ATC_SMEM);
-    attention_tc_kernel<false><<<grid, ATC_THREADS, ATC_SMEM, st>>>(*mh, *mh, cu, seqs, d, scale,
-                                                                      fmt, ch, cl, ldc, ovf);
+                         ATP_SMEM);
+    attention_tc_kernel<false><<<grid, ATP_THREADS, ATP_SMEM, st>>>(
+        *mh, *mh, cu, seqs, n_items, heads, d, scale, fmt, ch, cl, ldc, ovf);
   }
   return cudaGetLastError();
 }

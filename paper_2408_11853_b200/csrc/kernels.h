@@ -19,12 +19,12 @@ cudaError_t launch_attention(const uint16_t* qh, const uint16_t* ql, int ldq, in
                              const int32_t* cu,
                              const int2* work, int n_work, uint16_t* ch, uint16_t* cl,
                              int ldc, int fmt, int* ovf, cudaStream_t st);
-// tcgen05 attention, one CTA per (listed sequence, head); L <= 128, d_head == 64.
-// Maps: Q|K|V hi/lo [T][ldq] with box {64 cols, 16 rows}.
+// Persistent tcgen05 attention over (listed sequence, head) items; L <= 128,
+// d_head == 64. Maps: Q|K|V hi/lo [T][ldq] with box {64 cols, 16 rows}.
 cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml, bool split,
                                 const int32_t* cu, const int32_t* seqs, int n_seqs, int heads,
                                 int d, int fmt, uint16_t* ch, uint16_t* cl, int ldc, int* ovf,
-                                cudaStream_t st);
+                                int num_sms, cudaStream_t st);
 cudaError_t launch_features(const float* x, int ld, int d, int kind, const int32_t* cu, int n,
                             uint16_t* fh, uint16_t* fl, int ldf, int fmt, int* ovf,
                             cudaStream_t st);

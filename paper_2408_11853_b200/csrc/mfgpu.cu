@@ -415,7 +415,7 @@ struct mfg_ctx {
         int e = ev_begin();
         if (n_short > 0)
           CK(launch_attention_tc(&qmh16, split ? &qml16 : &qmh16, split, d_cu, d_short, n_short,
-                                 H, d, fmt, ca.hi, ca.lo, ca.ld, d_ovf, st));
+                                 H, d, fmt, ca.hi, ca.lo, ca.ld, d_ovf, num_sms, st));
         if (n_work > 0)
           CK(launch_attention(qa.hi, qa.lo, qa.ld, d, H, d_cu, d_work, (int)n_work, ca.hi, ca.lo,
                               ca.ld, fmt, d_ovf, st));
@@ -879,8 +879,11 @@ extern "C" int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* c
         throw Fail{MFG_ERR_RUNTIME, err};
       if (split && !make_tmap_u16(&m16l, ql, Tp, ldq, ldq, 16, err, sizeof err))
         throw Fail{MFG_ERR_RUNTIME, err};
+      int sms = 148, dev = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       CK(launch_attention_tc(&m16h, split ? &m16l : &m16h, split, dcu, dsh, (int)shorts.size(),
-                             n_heads, d, fmt, ch, cl, ldc, nullptr, 0));
+                             n_heads, d, fmt, ch, cl, ldc, nullptr, sms, 0));
     }
     if (!work.empty())
       CK(launch_attention(qh, ql, ldq, d, n_heads, dcu, dw, (int)work.size(), ch, cl, ldc, fmt,
