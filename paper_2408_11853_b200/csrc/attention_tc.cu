@@ -16,7 +16,8 @@
 // columns once S is dead) and softmax warp group, so one group's softmax runs
 // while the other waits for its P·V MMAs and the TMA/MMA of later items:
 //   warp 0 lane 0  TMA producer  (Q, K, V tiles, 16-row boxes, 128B swizzle)
-//   warp 1 lane 0  MMA issuer    (S(k), S(k+1), then O(k) as soon as P(k) lands)
+//   warp 1 lane 0  MMA issuer    (event loop: S(k) when its tiles land, O(k) when
+//                                 P(k) lands; neither queue blocks the other)
 //   warps 2-5 / 6-9  softmax (row = TMEM lane, two TMEM passes: max, exp) and
 //                  epilogue for the items of lane 0 / lane 1
 // P is written, swizzled K-major, into the item's (dead) Q/K smem tiles.
@@ -108,61 +109,74 @@ __global__ void __launch_bounds__(ATP_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
+    // Event loop over two queues so neither blocks the other: S(ks) as soon as
+    // its tiles landed and its TMEM region is free, O(ko) as soon as P(ko) landed.
     if (lane == 0) {
-      auto issue_s = [&](int it, int k) {
-        const int b = k & 1;
-        const uint32_t ph = (k >> 1) & 1;
-        const AttItem a = att_item(it, cu, seqs, heads);
-        const int n16 = (a.L + 15) & ~15;
-        mbar_wait(&t_empty[b], ph ^ 1);   // epilogue of item k-2 read its O
-        mbar_wait(&load_full[b], ph);
-        tc_fence_after();
-        const uint32_t idesc = idesc_f16kind(128, n16, fmt);
-        uint8_t* t = buf(b);
-        const uint64_t qh = umma_desc_sw128(t), kh = umma_desc_sw128(t + 2 * ATP_TILE);
-        const uint64_t ql = umma_desc_sw128(t + ATP_TILE), kl = umma_desc_sw128(t + 3 * ATP_TILE);
-        const uint32_t ts = tm + b * 128;
+      const int mine = blockIdx.x < n_items ? (n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+      int ks = 0, ko = 0;
+      uint32_t idle = 0;
+      while (ko < mine) {
+        bool progress = false;
+        if (ks < mine && ks < ko + 2) {
+          const int b = ks & 1;
+          const uint32_t ph = (ks >> 1) & 1;
+          if (mbar_test(&t_empty[b], ph ^ 1) && mbar_test(&load_full[b], ph)) {
+            tc_fence_after();
+            const AttItem a = att_item(blockIdx.x + ks * gridDim.x, cu, seqs, heads);
+            const int n16 = (a.L + 15) & ~15;
+            const uint32_t idesc = idesc_f16kind(128, n16, fmt);
+            uint8_t* t = buf(b);
+            const uint64_t qh = umma_desc_sw128(t), kh = umma_desc_sw128(t + 2 * ATP_TILE);
+            const uint64_t ql = umma_desc_sw128(t + ATP_TILE),
+                           kl = umma_desc_sw128(t + 3 * ATP_TILE);
+            const uint32_t ts = tm + b * 128;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t adv = (uint64_t)(kk * 32) >> 4;
-          tc_mma_bf16(ts, qh + adv, kh + adv, idesc, kk != 0);
-          if (SPLIT) {
-            tc_mma_bf16(ts, ql + adv, kh + adv, idesc, 1);
-            tc_mma_bf16(ts, qh + adv, kl + adv, idesc, 1);
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t adv = (uint64_t)(kk * 32) >> 4;
+              tc_mma_bf16(ts, qh + adv, kh + adv, idesc, kk != 0);
+              if (SPLIT) {
+                tc_mma_bf16(ts, ql + adv, kh + adv, idesc, 1);
+                tc_mma_bf16(ts, qh + adv, kl + adv, idesc, 1);
+              }
+            }
+            tc_commit(&s_full[b]);
+            ++ks;
+            progress = true;
           }
         }
-        tc_commit(&s_full[b]);
-      };
-      int k = 0;
-      int it = blockIdx.x;
-      if (it < n_items) issue_s(it, 0);
-      if (it + (int)gridDim.x < n_items) issue_s(it + gridDim.x, 1);
-      for (; it < n_items; it += gridDim.x, ++k) {
-        const int b = k & 1;
-        const uint32_t ph = (k >> 1) & 1;
-        const AttItem a = att_item(it, cu, seqs, heads);
-        const int n16 = (a.L + 15) & ~15;
-        mbar_wait(&p_full[b], ph);
-        tc_fence_after();
-        const uint32_t idesc = idesc_f16kind(128, 64, fmt) | (1u << 16);  // B MN-major
-        uint8_t* t = buf(b);
-        const uint32_t to = tm + b * 128;  // S is dead once P(k) landed
-        for (int kk = 0; kk < n16; kk += 16) {
-          const int atom = kk >> 6;
-          const uint64_t aoff = (uint64_t)((kk & 63) * 2) >> 4;
-          const uint64_t ph_ = umma_desc_sw128(t + atom * ATP_TILE) + aoff;
-          const uint64_t pl_ = umma_desc_sw128(t + (2 + atom) * ATP_TILE) + aoff;
-          const uint64_t vh = umma_desc_sw128(t + 4 * ATP_TILE + kk * 128);
-          const uint64_t vl = umma_desc_sw128(t + 5 * ATP_TILE + kk * 128);
-          tc_mma_bf16(to, ph_, vh, idesc, kk != 0);
-          if (SPLIT) {
-            tc_mma_bf16(to, pl_, vh, idesc, 1);
-            tc_mma_bf16(to, ph_, vl, idesc, 1);
+        if (ko < ks) {
+          const int b = ko & 1;
+          const uint32_t ph = (ko >> 1) & 1;
+          if (mbar_test(&p_full[b], ph)) {
+            tc_fence_after();
+            const AttItem a = att_item(blockIdx.x + ko * gridDim.x, cu, seqs, heads);
+            const int n16 = (a.L + 15) & ~15;
+            const uint32_t idesc = idesc_f16kind(128, 64, fmt) | (1u << 16);  // B MN-major
+            uint8_t* t = buf(b);
+            const uint32_t to = tm + b * 128;  // S is dead once P(ko) landed
+            for (int kk = 0; kk < n16; kk += 16) {
+              const int atom = kk >> 6;
+              const uint64_t aoff = (uint64_t)((kk & 63) * 2) >> 4;
+              const uint64_t ph_ = umma_desc_sw128(t + atom * ATP_TILE) + aoff;
+              const uint64_t pl_ = umma_desc_sw128(t + (2 + atom) * ATP_TILE) + aoff;
+              const uint64_t vh = umma_desc_sw128(t + 4 * ATP_TILE + kk * 128);
+              const uint64_t vl = umma_desc_sw128(t + 5 * ATP_TILE + kk * 128);
+              tc_mma_bf16(to, ph_, vh, idesc, kk != 0);
+              if (SPLIT) {
+                tc_mma_bf16(to, pl_, vh, idesc, 1);
+                tc_mma_bf16(to, ph_, vl, idesc, 1);
+              }
+            }
+            tc_commit(&o_full[b]);
+            ++ko;
+            progress = true;
           }
         }
-        tc_commit(&o_full[b]);
-        const int nxt2 = it + 2 * gridDim.x;
-        if (nxt2 < n_items) issue_s(nxt2, k + 2);  // waits for epilogue(k) to free region b
+        if (progress) {
+          idle = 0;
+        } else if (++idle > (1u << 27)) {
+          __trap();  // protocol bug: never hang the GPU
+        }
       }
     }
   } else {
