@@ -67,9 +67,14 @@ def prepare_model(cfg, rank, world, barrier):
     vocab = os.path.join(BENCH_DIR, f"config{cfg}.vocab.txt")
     done = path + ".ok"
     if env_int("LOCAL_RANK", 0) == 0 and not os.path.exists(done):
-        tensors = ((n, "f32", a.shape, a) for n, a in fx.synthetic_weights(man))
+        if cfg == 1:  # the reference fixture family (std-0.25 weights, 64-token vocab)
+            w = fx.fixture_weights(man, 1234)
+            tensors = [(n, "f32", w[n].shape, w[n]) for n, _ in fx.tensor_shapes(man)]
+            fx.write_vocab(vocab, fx.fixture_vocab_lines())
+        else:
+            tensors = ((n, "f32", a.shape, a) for n, a in fx.synthetic_weights(man))
+            fx.write_vocab(vocab, fx.synthetic_vocab_lines(man["vocab_size"]))
         write_container(ModelManifest(**man), tensors, path)
-        fx.write_vocab(vocab, fx.synthetic_vocab_lines(man["vocab_size"]))
         open(done, "w").close()
     barrier()
     while not os.path.exists(done):
@@ -146,30 +151,64 @@ def ncu_traffic():
     return None, None
 
 
-def cpu_baseline(cfg, n_records):
+def workload_lines(cfg, n, seed):
+    from oracle import fixtures as fx
+    if cfg == 1:
+        return fx.fixture_tsv_lines("comet", n, seed=seed)
+    return fx.synthetic_tsv_lines(cfg, n, seed=seed)
+
+
+def oracle_model(cfg):
+    from oracle import fixtures as fx
+    from oracle import tokenizer as otk
+    from oracle.encoder import OracleModel
+    man = dict(fx.CONFIGS[cfg])
+    if cfg == 1:
+        return OracleModel(man, fx.fixture_weights(man, 1234)), otk.OracleVocab(fx.fixture_vocab_lines())
+    return (OracleModel(man, dict(fx.synthetic_weights(man))),
+            otk.OracleVocab(fx.synthetic_vocab_lines(man["vocab_size"])))
+
+
+def cpu_baseline(cfg, n_records, return_scores=False):
     """Reference algorithm (oracle numpy port) on host cores, bounded sample."""
     from oracle import evaluate as oe
     from oracle import fixtures as fx
     from oracle import tokenizer as otk
     from oracle.encoder import OracleModel
 
-    man = dict(fx.CONFIGS[cfg])
-    weights = dict(fx.synthetic_weights(man))
-    model = OracleModel(man, weights)
-    vocab = otk.OracleVocab(fx.synthetic_vocab_lines(man["vocab_size"]))
-    lines = fx.synthetic_tsv_lines(cfg, n_records, seed=fx.TEXT_SEED + 777)
+    model, vocab = oracle_model(cfg)
+    lines = workload_lines(cfg, n_records, fx.TEXT_SEED + 777)
     oe.score_lines(model, vocab, lines[:1])  # discard run (BLAS warmup)
     t0 = time.perf_counter()
-    oe.score_lines(model, vocab, lines)
+    ref_scores, _ = oe.score_lines(model, vocab, lines)
     dt = time.perf_counter() - t0
     try:
         from threadpoolctl import threadpool_info
         cores = max((p.get("num_threads", 1) for p in threadpool_info()), default=1)
     except Exception:
         cores = os.cpu_count() or 1
-    return {"value": n_records / dt, "unit": UNIT, "cores": int(cores), "kind": "port",
-            "sample": f"{n_records} synthetic config-{cfg} records (oracle numpy port of "
-                      f"pkg/src/metricforge/encoder.py, fp32, {dt:.1f} s)"}
+    out = {"value": n_records / dt, "unit": UNIT, "cores": int(cores), "kind": "port",
+           "sample": f"{n_records} synthetic config-{cfg} records (oracle numpy port of "
+                     f"pkg/src/metricforge/encoder.py, fp32, {dt:.1f} s)"}
+    return (out, lines, ref_scores) if return_scores else out
+
+
+def parity_report(path, vocab_path, lines, ref, device):
+    """Same records through the device path at every precision vs the fp32
+    oracle (the reference algorithm): max/mean |delta| and Pearson."""
+    import paper_2408_11853_b200 as mf
+    ref = np.asarray(ref, dtype=np.float64)
+    out = {"n_records": len(lines), "tolerance": 1e-3, "reference": "oracle fp32 (numpy port)"}
+    for prec in ("fp32", "bf16x3", "bf16"):
+        cfg = mf.EvaluatorConfig(model=path, vocab=vocab_path, quiet=True, validate=False,
+                                 device=device, precision=prec)
+        with mf.Evaluator(cfg) as ev:
+            got = np.asarray(ev.evaluate_lines(lines).segment_scores, dtype=np.float64)
+        d = np.abs(got - ref)
+        pear = float(np.corrcoef(got, ref)[0, 1]) if len(got) > 2 and ref.std() > 0 else None
+        out[prec] = {"max_abs": float(d.max()), "mean_abs": float(d.mean()), "pearson": pear}
+    out["fp32_within_tolerance"] = out["fp32"]["max_abs"] <= 1e-3
+    return out
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -183,10 +222,8 @@ def run_reference(args, rank, world):
     from oracle import tokenizer as otk
     from oracle.encoder import OracleModel
 
-    man = dict(fx.CONFIGS[args.config])
-    model = OracleModel(man, dict(fx.synthetic_weights(man)))
-    vocab = otk.OracleVocab(fx.synthetic_vocab_lines(man["vocab_size"]))
-    lines = fx.synthetic_tsv_lines(args.config, per_step * (args.steps + args.warmup), seed=fx.TEXT_SEED)
+    model, vocab = oracle_model(args.config)
+    lines = workload_lines(args.config, per_step * (args.steps + args.warmup), fx.TEXT_SEED)
     chunks = [lines[i * per_step:(i + 1) * per_step] for i in range(args.steps + args.warmup)]
     for c in chunks[:args.warmup]:
         oe.score_lines(model, vocab, c)
@@ -227,7 +264,7 @@ def run_ours(args, rank, world, local_rank):
     man, path, vocab_path = prepare_model(args.config, rank, world, barrier)
     n_steps = args.steps + args.warmup
     R = args.records_per_step
-    lines = fx.synthetic_tsv_lines(args.config, R * n_steps, seed=fx.TEXT_SEED + 1000 * rank)
+    lines = workload_lines(args.config, R * n_steps, fx.TEXT_SEED + 1000 * rank)
 
     # ---------------- device-resident timing (value)
     model = mf.GpuScoringModel(path, device=local_rank, precision=args.precision,
@@ -338,9 +375,9 @@ def run_ours(args, rank, world, local_rank):
         "scaling": "weak", "vs_baseline": None,
         "dtype": {"fp32": "fp16x3-split (fp32-parity)", "bf16x3": "bf16x3-split",
                   "bf16": "bf16"}[args.precision],
-        "data": "synthetic (SURVEY §8d generator; random-init N(0,0.02) weights)",
-        "config": {"workload": f"config {args.config}: " + fx.CONFIG_NAMES[args.config] +
-                               ", COMET triplets, content len ~U{1..126}/field",
+        "data": ("synthetic (reference fixture generator, std-0.25 fixture weights)" if args.config == 1
+                 else "synthetic (SURVEY §8d generator; random-init N(0,0.02) weights)"),
+        "config": {"workload": f"config {args.config}: " + fx.CONFIG_NAMES[args.config],
                    "model": "XLM-R-large-shaped encoder (24 x d1024 x h16 x ffn4096) + "
                             "head [6144,3072,1024,1]" if args.config == 2 else fx.CONFIG_NAMES[args.config],
                    "records_per_step": R, "tokens_per_step": sum(tokens_per_step[args.warmup:]) / args.steps,
@@ -354,7 +391,9 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_records)
+        base, ref_lines, ref = cpu_baseline(args.config, args.cpu_records, return_scores=True)
+        line["cpu_baseline"] = base
+        line["parity"] = parity_report(path, vocab_path, ref_lines, ref, local_rank)
     print(json.dumps(line), flush=True)
 
 
