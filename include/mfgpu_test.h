@@ -23,6 +23,11 @@ int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, int32_t K, c
 int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* cu, int32_t d,
                    int32_t n_heads, const float* qkv, float* ctx_out, int32_t use_tc);
 
+/* Diagnostics: enable = 1 starts recording a clock64 trace of the tcgen05
+ * attention kernel (first 4 CTAs x 64 items x 8 events); enable = 0 stops and
+ * copies it to host_out[2048]. */
+int mfgt_att_trace(int32_t enable, long long* host_out);
+
 /* out[T][d] = LayerNorm(y) with gain g and bias b (eps 1e-5). */
 int mfgt_layernorm(int32_t T, int32_t d, const float* y, const float* g, const float* b,
                    float* out);

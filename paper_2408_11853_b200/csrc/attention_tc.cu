@@ -1,285 +1,375 @@
-// Persistent tcgen05 attention for sequences of <= 128 tokens with d_head 64
-// (XLM-R / InfoXLM / RemBERT shapes: every record of configs 2-4). Replaces the
+// Persistent tcgen05 attention over packed 128-token tiles, d_head 64
+// (XLM-R / InfoXLM / RemBERT shapes: every sequence of configs 2-4). Replaces the
 // per-head loop of `pkg/src/metricforge/encoder.py:132-147` (+ masked_softmax 60-66).
 //
-// Work item = (sequence, head). Per item:
-//   S = Q·Kᵀ      tcgen05.mma M=128 x N=round16(L) x K=64 -> fp32 in TMEM
-//   P = exp(S·scale - rowmax) = exp2f((S - rowmax)·scale·log2e) in fp32, keys >= L
-//       get exactly 0
-//   O = P·V       tcgen05.mma M=128 x N=64 x K=round16(L), V is an MN-major B
-//   ctx = O / rowsum -> 16-bit hi/lo pieces (the O-projection's A operand)
-// Operands are 16-bit hi/lo pairs and each product is three MMAs
-// (hi·hi + lo·hi + hi·lo), like the GEMMs (~22 significant bits with fp16).
+// Tiles. The host packs whole sequences (each <= 128 tokens) greedily into tiles
+// of <= 128 consecutive rows of the token-packed stream (`att_plan_tiles`). A work
+// item is (tile, head); its S = Q·Kᵀ is block-diagonal: row r may only attend to
+// the keys of its own sequence, [rng[t].x, rng[t].y) (`token_ranges_kernel`),
+// every other key gets exactly 0 weight — which is the reference's per-sequence
+// masked softmax, so sequences never mix and padding never exists.
 //
-// One CTA per SM walks items round-robin. Items alternate between two lanes
-// b = k & 1, each with its own smem buffer, TMEM region (S, then O in the same
-// columns once S is dead) and softmax warp group, so one group's softmax runs
-// while the other waits for its P·V MMAs and the TMA/MMA of later items:
-//   warp 0 lane 0  TMA producer  (Q, K, V tiles, 16-row boxes, 128B swizzle)
-//   warp 1 lane 0  MMA issuer    (event loop: S(k) when its tiles land, O(k) when
-//                                 P(k) lands; neither queue blocks the other)
-//   warps 2-5 / 6-9  softmax (row = TMEM lane, two TMEM passes: max, exp) and
-//                  epilogue for the items of lane 0 / lane 1
-// P is written, swizzled K-major, into the item's (dead) Q/K smem tiles.
+// Per item:
+//   S = Q·Kᵀ      tcgen05.mma M=128 x N=round16(n) x K=64, Q/K from smem (TMA)
+//   P = exp(S·scale - rowmax) over the row's own keys, 0 elsewhere, fp32 math,
+//       written back into S's TMEM columns as 16-bit pieces (P never touches smem)
+//   O = P·V       tcgen05.mma M=128 x N=64 x K=round16(n), A = P from TMEM,
+//                 B = V (MN-major) from smem
+//   ctx = O / rowsum -> 16-bit hi/lo pieces (the O-projection's A operand)
+// With SPLIT every product is three MMAs (hi·hi + lo·hi + hi·lo) of fp16 (or
+// bf16) pieces, like the GEMMs (~22 significant bits with fp16).
+//
+// Roles (576 threads, one CTA per SM, items round-robin):
+//   warp 0       TMA producer: Q|K ring (QK_ST stages) and V ring (V_ST stages)
+//   warp 1       MMA issuer:   event loop over S(ks) and O(ko)
+//   warps 2-9    group 0 (items k even, TMEM region 0): softmax, then epilogue
+//   warps 10-17  group 1 (items k odd,  TMEM region 1)
+// Inside a group two warps share each TMEM lane quarter (= 32 tile rows): warp
+// half hf takes the key chunks c with c % 2 == hf and the O columns 32hf..+31;
+// the pair exchanges row max / row sum through TMEM (named barrier).
+// TMEM columns: S/P of region b at 128b..128b+127; O of region b at 256+64b;
+// partial max / sum of region b, half hf at 384+4b+hf / 384+4b+2+hf.
+// Measured (tools/mma_probe.cu): a 128xNx16 MMA costs >= ~72 cycles (SS) /
+// ~107 cycles (A from TMEM) for N <= 128, so per item the tensor pipe needs
+// ~1.1k cycles for S and ~2.5k for O.
+// P layout in TMEM (A operand, K-major, two 16-bit values per 32-bit column):
+// keys 32c..32c+31 -> hi pieces in columns 32c..32c+15, lo pieces in 32c+16..+31,
+// i.e. exactly the columns of S chunk c that the same thread just consumed.
+#include <vector>
+
 #include "kernels.h"
 #include "ptx.cuh"
 
 namespace mfg {
 
-constexpr int ATP_THREADS = 320;
-constexpr int ATP_TILE = 128 * 128;            // one 128-row x 64-col 16-bit tile
-constexpr int ATP_BUF = 6 * ATP_TILE;          // Qh Ql Kh Kl Vh Vl
-constexpr int ATP_SMEM = 1024 + 2 * ATP_BUF + 256;
-
-struct AttItem {
-  int start, L, h;
-};
-
-__device__ __forceinline__ AttItem att_item(int it, const int32_t* cu, const int32_t* seqs,
-                                            int heads) {
-  const int s = seqs[it / heads];
-  AttItem a;
-  a.start = cu[s];
-  a.L = cu[s + 1] - a.start;
-  a.h = it % heads;
-  return a;
-}
+constexpr int ATQ_THREADS = 576;
+constexpr int ATQ_TILE = 128 * 128;  // 128 rows x 64 cols of 16-bit values (128B swizzle)
 
 template <bool SPLIT>
-__global__ void __launch_bounds__(ATP_THREADS, 1)
+struct AtqCfg {
+  static constexpr int QK_BYTES = (SPLIT ? 4 : 2) * ATQ_TILE;  // Qh Kh (Ql Kl)
+  static constexpr int V_BYTES = (SPLIT ? 2 : 1) * ATQ_TILE;   // Vh (Vl)
+  static constexpr int QK_ST = SPLIT ? 2 : 3;
+  static constexpr int V_ST = SPLIT ? 3 : 6;
+  static constexpr int BAR_OFF = QK_ST * QK_BYTES + V_ST * V_BYTES;
+  static constexpr int SMEM = 1024 + BAR_OFF + 256;
+  static_assert(SMEM <= 232448, "attention smem");
+};
+
+__device__ __forceinline__ void tmem_st_8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_1(uint32_t taddr, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ float tmem_ld_1(uint32_t taddr) {
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return __uint_as_float(v);
+}
+__device__ __forceinline__ void tc_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem], kind::f16.
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Optional per-item clock64 trace of the first 4 CTAs (diagnostics only,
+// tools/att_trace.py): [cta][item][event], events S-issued, O-issued,
+// S-seen, P-done, O-seen (epilogue), item-done (epilogue).
+__device__ long long* g_att_trace = nullptr;
+#define ATT_TRACE(k, ev)                                              \
+  do {                                                                \
+    if (g_att_trace && blockIdx.x < 4 && (k) < 64)                    \
+      g_att_trace[(blockIdx.x * 64 + (k)) * 8 + (ev)] = clock64();    \
+  } while (0)
+
+template <bool SPLIT>
+__global__ void __launch_bounds__(ATQ_THREADS, 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap mh,
-                        const __grid_constant__ CUtensorMap ml, const int32_t* __restrict__ cu,
-                        const int32_t* __restrict__ seqs, int n_items, int heads, int d,
-                        float scale, int fmt, uint16_t* __restrict__ ch,
-                        uint16_t* __restrict__ cl, int ldc, int* ovf) {
+                        const __grid_constant__ CUtensorMap ml, const int2* __restrict__ tiles,
+                        const int2* __restrict__ rng, int n_items, int heads, int d, float scale,
+                        int fmt, uint16_t* __restrict__ ch, uint16_t* __restrict__ cl, int ldc) {
+  using C = AtqCfg<SPLIT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 2 * ATP_BUF);
-  uint64_t* load_full = bars;       // [2]
-  uint64_t* s_full = bars + 2;      // [2]
-  uint64_t* p_full = bars + 4;      // [2]
-  uint64_t* o_full = bars + 6;      // [2]  also: smem buffer free again
-  uint64_t* t_empty = bars + 8;     // [2]  TMEM (S, O) buffer free again
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
+  uint64_t* qk_full = bars;                 // [QK_ST]
+  uint64_t* qk_empty = qk_full + C::QK_ST;  // [QK_ST]
+  uint64_t* v_full = qk_empty + C::QK_ST;   // [V_ST]
+  uint64_t* v_empty = v_full + C::V_ST;     // [V_ST]
+  uint64_t* s_full = v_empty + C::V_ST;     // [2]  S(k) in region k&1
+  uint64_t* p_full = s_full + 2;            // [2]  P(k) written (256 group threads)
+  uint64_t* o_full = p_full + 2;            // [2]  O(k) done (also: P region free)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_full + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
+    for (int s = 0; s < C::QK_ST; ++s) {
+      mbar_init(&qk_full[s], 1);
+      mbar_init(&qk_empty[s], 1);
+    }
+    for (int s = 0; s < C::V_ST; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&load_full[b], 1);
       mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 4);
+      mbar_init(&p_full[b], 256);
       mbar_init(&o_full[b], 1);
-      mbar_init(&t_empty[b], 4);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<256>(tslot);
+  if (warp == 1) tmem_alloc<512>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tm = *tslot;
-  auto buf = [&](int b) { return sm + b * ATP_BUF; };
+  const int mine = blockIdx.x < n_items ? (n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto item_of = [&](int k) { return blockIdx.x + k * gridDim.x; };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      int k = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++k) {
-        const int b = k & 1;
-        const uint32_t ph = (k >> 1) & 1;
-        const AttItem a = att_item(it, cu, seqs, heads);
-        const int n16 = (a.L + 15) & ~15;
-        mbar_wait(&o_full[b], ph ^ 1);  // item k-2 finished reading this buffer
-        mbar_expect_tx(&load_full[b], (uint32_t)n16 * 128 * (SPLIT ? 6 : 3));
-        const int cq = a.h * 64, ck = d + a.h * 64, cv = 2 * d + a.h * 64;
-        uint8_t* t = buf(b);
-        for (int r0 = 0; r0 < n16; r0 += 16) {
-          const int so = r0 * 128;
-          tma_load_2d(t + 0 * ATP_TILE + so, &mh, &load_full[b], cq, a.start + r0);
-          tma_load_2d(t + 2 * ATP_TILE + so, &mh, &load_full[b], ck, a.start + r0);
-          tma_load_2d(t + 4 * ATP_TILE + so, &mh, &load_full[b], cv, a.start + r0);
+      tma_prefetch(&mh);
+      if (SPLIT) tma_prefetch(&ml);
+      for (int k = 0; k < mine; ++k) {
+        const int it = item_of(k);
+        const int2 tl = tiles[it / heads];
+        const int h = it % heads;
+        const int cq = h * 64, ck = d + h * 64, cv = 2 * d + h * 64;
+        {
+          const int s = k % C::QK_ST;
+          mbar_wait(&qk_empty[s], ((k / C::QK_ST) & 1) ^ 1);
+          mbar_expect_tx(&qk_full[s], C::QK_BYTES);
+          uint8_t* t = sm + s * C::QK_BYTES;
+          tma_load_2d(t, &mh, &qk_full[s], cq, tl.x);
+          tma_load_2d(t + ATQ_TILE, &mh, &qk_full[s], ck, tl.x);
           if (SPLIT) {
-            tma_load_2d(t + 1 * ATP_TILE + so, &ml, &load_full[b], cq, a.start + r0);
-            tma_load_2d(t + 3 * ATP_TILE + so, &ml, &load_full[b], ck, a.start + r0);
-            tma_load_2d(t + 5 * ATP_TILE + so, &ml, &load_full[b], cv, a.start + r0);
+            tma_load_2d(t + 2 * ATQ_TILE, &ml, &qk_full[s], cq, tl.x);
+            tma_load_2d(t + 3 * ATQ_TILE, &ml, &qk_full[s], ck, tl.x);
           }
+        }
+        {
+          const int s = k % C::V_ST;
+          mbar_wait(&v_empty[s], ((k / C::V_ST) & 1) ^ 1);
+          mbar_expect_tx(&v_full[s], C::V_BYTES);
+          uint8_t* t = sm + C::QK_ST * C::QK_BYTES + s * C::V_BYTES;
+          tma_load_2d(t, &mh, &v_full[s], cv, tl.x);
+          if (SPLIT) tma_load_2d(t + ATQ_TILE, &ml, &v_full[s], cv, tl.x);
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    // Event loop over two queues so neither blocks the other: S(ks) as soon as
-    // its tiles landed and its TMEM region is free, O(ko) as soon as P(ko) landed.
     if (lane == 0) {
-      const int mine = blockIdx.x < n_items ? (n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+      // Event loop: S(ks) as soon as its Q/K tiles landed and its TMEM region is
+      // free, O(ko) as soon as P(ko) and V(ko) are ready (P(k) also implies
+      // that the group finished reading O(k-2)).
+      auto issue_s = [&](int k) {
+        const int b = k & 1;
+        const int2 tl = tiles[item_of(k) / heads];
+        const int n16 = (tl.y + 15) & ~15;
+        const int s = k % C::QK_ST;
+        const uint32_t idesc = idesc_f16kind(128, n16, fmt);
+        uint8_t* t = sm + s * C::QK_BYTES;
+        const uint64_t qh = umma_desc_sw128(t), kh = umma_desc_sw128(t + ATQ_TILE);
+        const uint64_t ql = umma_desc_sw128(t + 2 * ATQ_TILE),
+                       kl = umma_desc_sw128(t + 3 * ATQ_TILE);
+        const uint32_t ts = tm + b * 128;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t adv = (uint64_t)(kk * 32) >> 4;
+          tc_mma_bf16(ts, qh + adv, kh + adv, idesc, kk != 0);
+          if (SPLIT) {
+            tc_mma_bf16(ts, ql + adv, kh + adv, idesc, 1);
+            tc_mma_bf16(ts, qh + adv, kl + adv, idesc, 1);
+          }
+        }
+        tc_commit(&s_full[b]);
+        tc_commit(&qk_empty[s]);
+      };
+      auto issue_o = [&](int k) {
+        const int b = k & 1;
+        const int2 tl = tiles[item_of(k) / heads];
+        const int n16 = (tl.y + 15) & ~15;
+        const int s = k % C::V_ST;
+        const uint32_t idesc = idesc_f16kind(128, 64, fmt) | (1u << 16);  // B MN-major
+        uint8_t* t = sm + C::QK_ST * C::QK_BYTES + s * C::V_BYTES;
+        const uint32_t tp = tm + b * 128, to = tm + 256 + b * 64;
+        for (int kk = 0; kk < n16; kk += 16) {
+          const uint32_t ph_ = tp + 32 * (kk >> 5) + 8 * ((kk >> 4) & 1);
+          const uint64_t vh = umma_desc_sw128(t + kk * 128);
+          tc_mma_ts(to, ph_, vh, idesc, kk != 0);
+          if (SPLIT) {
+            const uint64_t vl = umma_desc_sw128(t + ATQ_TILE + kk * 128);
+            tc_mma_ts(to, ph_ + 16, vh, idesc, 1);
+            tc_mma_ts(to, ph_, vl, idesc, 1);
+          }
+        }
+        tc_commit(&o_full[b]);
+        tc_commit(&v_empty[s]);
+      };
       int ks = 0, ko = 0;
-      uint32_t idle = 0;
+      const long long t0 = clock64();
       while (ko < mine) {
         bool progress = false;
-        if (ks < mine && ks < ko + 2) {
-          const int b = ks & 1;
-          const uint32_t ph = (ks >> 1) & 1;
-          if (mbar_test(&t_empty[b], ph ^ 1) && mbar_test(&load_full[b], ph)) {
-            tc_fence_after();
-            const AttItem a = att_item(blockIdx.x + ks * gridDim.x, cu, seqs, heads);
-            const int n16 = (a.L + 15) & ~15;
-            const uint32_t idesc = idesc_f16kind(128, n16, fmt);
-            uint8_t* t = buf(b);
-            const uint64_t qh = umma_desc_sw128(t), kh = umma_desc_sw128(t + 2 * ATP_TILE);
-            const uint64_t ql = umma_desc_sw128(t + ATP_TILE),
-                           kl = umma_desc_sw128(t + 3 * ATP_TILE);
-            const uint32_t ts = tm + b * 128;
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const uint64_t adv = (uint64_t)(kk * 32) >> 4;
-              tc_mma_bf16(ts, qh + adv, kh + adv, idesc, kk != 0);
-              if (SPLIT) {
-                tc_mma_bf16(ts, ql + adv, kh + adv, idesc, 1);
-                tc_mma_bf16(ts, qh + adv, kl + adv, idesc, 1);
-              }
-            }
-            tc_commit(&s_full[b]);
-            ++ks;
-            progress = true;
-          }
+        if (ks < mine && ks <= ko + 1 &&
+            (ks < 2 || mbar_test(&o_full[ks & 1], ((ks - 2) >> 1) & 1)) &&
+            mbar_test(&qk_full[ks % C::QK_ST], (ks / C::QK_ST) & 1)) {
+          tc_fence_after();
+          ATT_TRACE(ks, 0);
+          issue_s(ks++);
+          progress = true;
         }
-        if (ko < ks) {
-          const int b = ko & 1;
-          const uint32_t ph = (ko >> 1) & 1;
-          if (mbar_test(&p_full[b], ph)) {
-            tc_fence_after();
-            const AttItem a = att_item(blockIdx.x + ko * gridDim.x, cu, seqs, heads);
-            const int n16 = (a.L + 15) & ~15;
-            const uint32_t idesc = idesc_f16kind(128, 64, fmt) | (1u << 16);  // B MN-major
-            uint8_t* t = buf(b);
-            const uint32_t to = tm + b * 128;  // S is dead once P(ko) landed
-            for (int kk = 0; kk < n16; kk += 16) {
-              const int atom = kk >> 6;
-              const uint64_t aoff = (uint64_t)((kk & 63) * 2) >> 4;
-              const uint64_t ph_ = umma_desc_sw128(t + atom * ATP_TILE) + aoff;
-              const uint64_t pl_ = umma_desc_sw128(t + (2 + atom) * ATP_TILE) + aoff;
-              const uint64_t vh = umma_desc_sw128(t + 4 * ATP_TILE + kk * 128);
-              const uint64_t vl = umma_desc_sw128(t + 5 * ATP_TILE + kk * 128);
-              tc_mma_bf16(to, ph_, vh, idesc, kk != 0);
-              if (SPLIT) {
-                tc_mma_bf16(to, pl_, vh, idesc, 1);
-                tc_mma_bf16(to, ph_, vl, idesc, 1);
-              }
-            }
-            tc_commit(&o_full[b]);
-            ++ko;
-            progress = true;
-          }
+        if (ko < ks && mbar_test(&p_full[ko & 1], (ko >> 1) & 1) &&
+            mbar_test(&v_full[ko % C::V_ST], (ko / C::V_ST) & 1)) {
+          tc_fence_after();
+          ATT_TRACE(ko, 1);
+          issue_o(ko++);
+          progress = true;
         }
-        if (progress) {
-          idle = 0;
-        } else if (++idle > (1u << 27)) {
-          __trap();  // protocol bug: never hang the GPU
+        if (!progress) {
+          __nanosleep(20);
+          if (clock64() - t0 > (1ll << 36)) __trap();  // protocol bug: never hang the GPU
         }
       }
     }
   } else {
     // ------------------------------------------------------------ softmax + epilogue
-    const int g = (warp - 2) >> 2;   // lane (buffer) this group serves: items k = g, g+2, ...
-    const int q = warp & 3;          // TMEM lane quarter
-    const int r = q * 32 + lane;     // query row owned by this thread
+    const int g = (warp - 2) >> 3;          // group = region = item parity
+    const int hf = ((warp - 2) >> 2) & 1;   // which half of the key chunks
+    const int q = warp & 3;                 // TMEM lane quarter
+    const int r = q * 32 + lane;            // tile row owned by this thread
+    const int pair_bar = 1 + g * 4 + q;     // named barrier of the two warps of this quarter
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const uint32_t tmax = tm + lane_off + 384 + 4 * g;
     const float c2 = scale * 1.4426950408889634f;  // exp(x*scale) = 2^(x*c2)
-    int j = 0;
-    for (int it = blockIdx.x + g * gridDim.x; it < n_items; it += 2 * gridDim.x, ++j) {
+    for (int k = g; k < mine; k += 2) {
       const int b = g;
-      const uint32_t ph = j & 1;
-      const AttItem a = att_item(it, cu, seqs, heads);
-      const bool active = q * 32 < a.L;  // warp-uniform: warp owns >= 1 real row
-      const uint32_t trow = tm + b * 128 + ((uint32_t)(q * 32) << 16);
-      // ---- softmax: S row -> registers (single TMEM pass) -> P pieces in smem
-      mbar_wait(&s_full[b], ph);
+      const int it = item_of(k);
+      const int2 tl = tiles[it / heads];
+      const int h = it % heads;
+      const int n = tl.y, n16 = (n + 15) & ~15;
+      int ks = 0, ke = 0;
+      if (r < n) {
+        const int2 rr = rng[tl.x + r];
+        ks = rr.x - tl.x;
+        ke = rr.y - tl.x;
+      }
+      mbar_wait(&s_full[b], (k >> 1) & 1);
+      const bool tr = hf == 0 && q == 0 && lane == 0;
+      if (tr) ATT_TRACE(k, 2);
       tc_fence_after();
+      const bool active = q * 32 < n;  // warp-uniform (same for both warps of the pair)
       float sum = 1.f;
       if (active) {
-        // two TMEM passes (max, then exp) keep the row out of registers
-        const int nchunk = (a.L + 31) >> 5;
-        float mx = -INFINITY;
-        for (int c = 0; c < nchunk; ++c) {
-          float v[32];
-          tmem_ld_32x32(trow + c * 32, v);
+        const uint32_t trow = tm + b * 128 + lane_off;
+        int lo = r < n ? ks : 1 << 20, hi = r < n ? ke : 0;
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c * 32 + i < a.L) mx = fmaxf(mx, v[i]);
+        for (int o = 16; o > 0; o >>= 1) {
+          lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+          hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
         }
+        const int c_lo = lo >> 5, c_hi = (hi - 1) >> 5, c_end = (n16 + 31) >> 5;
+        const bool use[2] = {hf >= c_lo && hf <= c_hi, hf + 2 >= c_lo && hf + 2 <= c_hi};
+        float mx = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (use[j]) {
+            float v[32];
+            tmem_ld_32x32(trow + (hf + 2 * j) * 32, v);
+            const int a = ks - (hf + 2 * j) * 32, e = ke - (hf + 2 * j) * 32;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i >= a && i < e) mx = fmaxf(mx, v[i]);
+          }
+        }
+        tmem_st_1(tmax + hf, __float_as_uint(mx));
+        tc_wait_st();
+        tc_fence_before();
+        asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+        tc_fence_after();
+        mx = fmaxf(mx, tmem_ld_1(tmax + (hf ^ 1)));
+        const float mxc = mx * c2;
         sum = 0.f;
-        uint8_t* t = buf(b);
-        for (int c = 0; c < nchunk; ++c) {
-          float v[32];
-          tmem_ld_32x32(trow + c * 32, v);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int c = hf + 2 * j;
+          if (c < c_end) {
+            float v[32];
+            if (use[j]) tmem_ld_32x32(trow + c * 32, v);
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              uint32_t hh[8], ll[8];
+              if (use[j]) {
+                const int a = ks - c * 32 - half * 16, e = ke - c * 32 - half * 16;
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) {
+                  const float x0 = v[half * 16 + i], x1 = v[half * 16 + i + 1];
+                  const float p0 = (i >= a && i < e) ? fast_exp2(fmaf(x0, c2, -mxc)) : 0.f;
+                  const float p1 =
+                      (i + 1 >= a && i + 1 < e) ? fast_exp2(fmaf(x1, c2, -mxc)) : 0.f;
+                  sum += p0 + p1;
+                  split2(p0, p1, fmt, hh[i / 2], ll[i / 2]);
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) hh[i] = ll[i] = 0u;
+              }
+              tmem_st_8(trow + c * 32 + half * 8, hh);
+              if (SPLIT) tmem_st_8(trow + c * 32 + 16 + half * 8, ll);
+            }
+          }
+        }
+      }
+      if (active) {
+        tmem_st_1(tmax + 2 + hf, __float_as_uint(sum));
+        tc_wait_st();
+        tc_fence_before();
+        asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+      }
+      tc_fence_before();
+      mbar_arrive(&p_full[b]);
+      if (tr) ATT_TRACE(k, 3);
+      // ---- epilogue: O columns 32hf..32hf+31 / rowsum -> ctx pieces
+      mbar_wait(&o_full[b], (k >> 1) & 1);
+      if (tr) ATT_TRACE(k, 4);
+      tc_fence_after();
+      if (active) {
+        float v[32];
+        tmem_ld_32x32(tm + lane_off + 256 + b * 64 + hf * 32, v);
+        const float inv = 1.0f / (tmem_ld_1(tmax + 2) + tmem_ld_1(tmax + 3));
+        if (r < n) {
+          // ctx is a convex combination of range-checked V rows: no fp16 overflow possible
+          const size_t ob = (size_t)(tl.x + r) * ldc + h * 64 + hf * 32;
           uint32_t hh[16], ll[16];
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            float p0 = 0.f, p1 = 0.f;
-            if (c * 32 + i < a.L) p0 = exp2f((v[i] - mx) * c2);
-            if (c * 32 + i + 1 < a.L) p1 = exp2f((v[i + 1] - mx) * c2);
-            sum += p0 + p1;
-            uint16_t h0, l0, h1, l1;
-            split16(p0, fmt, h0, l0);
-            split16(p1, fmt, h1, l1);
-            hh[i / 2] = h0 | ((uint32_t)h1 << 16);
-            ll[i / 2] = l0 | ((uint32_t)l1 << 16);
-          }
-          uint8_t* hi_atom = t + (c >> 1) * ATP_TILE;
-          uint8_t* lo_atom = t + (2 + (c >> 1)) * ATP_TILE;
+          for (int i = 0; i < 32; i += 2) split2(v[i] * inv, v[i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int unit = (c & 1) * 4 + u;
-            const uint32_t off = r * 128 + ((unit ^ (r & 7)) << 4);
-            *reinterpret_cast<uint4*>(hi_atom + off) =
+            *reinterpret_cast<uint4*>(ch + ob + 8 * u) =
                 make_uint4(hh[4 * u], hh[4 * u + 1], hh[4 * u + 2], hh[4 * u + 3]);
             if (SPLIT)
-              *reinterpret_cast<uint4*>(lo_atom + off) =
+              *reinterpret_cast<uint4*>(cl + ob + 8 * u) =
                   make_uint4(ll[4 * u], ll[4 * u + 1], ll[4 * u + 2], ll[4 * u + 3]);
           }
         }
-        // generic-proxy smem writes of P -> visible to the tensor core
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       }
       tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[b]);
-      // ---- epilogue: O row / rowsum -> ctx pieces
-      mbar_wait(&o_full[b], ph);
-      tc_fence_after();
-      if (active) {
-        const float inv = 1.0f / sum;
-        const size_t ob = (size_t)(a.start + r) * ldc + a.h * 64;
-        bool ok = true;
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          float v[32];
-          tmem_ld_32x32(trow + c * 32, v);
-          if (r < a.L) {
-            uint32_t hh[16], ll[16];
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              uint16_t h0, l0, h1, l1;
-              ok &= split16(v[i] * inv, fmt, h0, l0);
-              ok &= split16(v[i + 1] * inv, fmt, h1, l1);
-              hh[i / 2] = h0 | ((uint32_t)h1 << 16);
-              ll[i / 2] = l0 | ((uint32_t)l1 << 16);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              *reinterpret_cast<uint4*>(ch + ob + c * 32 + 8 * u) =
-                  make_uint4(hh[4 * u], hh[4 * u + 1], hh[4 * u + 2], hh[4 * u + 3]);
-              if (SPLIT)
-                *reinterpret_cast<uint4*>(cl + ob + c * 32 + 8 * u) =
-                    make_uint4(ll[4 * u], ll[4 * u + 1], ll[4 * u + 2], ll[4 * u + 3]);
-            }
-          }
-        }
-        if (!ok && ovf) atomicOr(ovf, 1);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&t_empty[b]);
+      if (tr) ATT_TRACE(k, 5);
     }
   }
 
@@ -287,28 +377,68 @@ __global__ void __launch_bounds__(ATP_THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<256>(tm);
+    tmem_dealloc<512>(tm);
   }
 }
 
+// rng[t] = [start, end) of the sequence containing token t (one CTA per sequence).
+__global__ void token_ranges_kernel(const int32_t* __restrict__ cu, int2* __restrict__ rng) {
+  const int a = cu[blockIdx.x], e = cu[blockIdx.x + 1];
+  for (int t = a + threadIdx.x; t < e; t += blockDim.x) rng[t] = make_int2(a, e);
+}
+
+cudaError_t att_set_trace(long long* dev_buf) {
+  return cudaMemcpyToSymbol(g_att_trace, &dev_buf, sizeof(dev_buf));
+}
+
+cudaError_t launch_token_ranges(const int32_t* cu, int nseq, int2* rng, cudaStream_t st) {
+  if (nseq <= 0) return cudaSuccess;
+  token_ranges_kernel<<<nseq, 128, 0, st>>>(cu, rng);
+  return cudaGetLastError();
+}
+
+void att_plan_tiles(const int32_t* cu, int nseq, bool tc_ok, std::vector<int2>& tiles,
+                    std::vector<int2>& work) {
+  tiles.clear();
+  work.clear();
+  int t0 = -1, n = 0;
+  for (int s = 0; s < nseq; ++s) {
+    const int a = cu[s], L = cu[s + 1] - a;
+    if (!tc_ok || L > 128) {
+      for (int q = 0; q < L; q += 64) work.push_back(make_int2(s, q));
+      continue;
+    }
+    if (t0 >= 0 && a == t0 + n && n + L <= 128) {
+      n += L;
+    } else {
+      if (t0 >= 0) tiles.push_back(make_int2(t0, n));
+      t0 = a;
+      n = L;
+    }
+  }
+  if (t0 >= 0) tiles.push_back(make_int2(t0, n));
+}
+
 cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml, bool split,
-                                const int32_t* cu, const int32_t* seqs, int n_seqs, int heads,
-                                int d, int fmt, uint16_t* ch, uint16_t* cl, int ldc, int* ovf,
+                                const int2* tiles, int n_tiles, const int2* rng, int heads, int d,
+                                int fmt, uint16_t* ch, uint16_t* cl, int ldc, int* ovf,
                                 int num_sms, cudaStream_t st) {
-  if (n_seqs <= 0) return cudaSuccess;
+  if (n_tiles <= 0) return cudaSuccess;
   const float scale = 1.0f / sqrtf((float)d / (float)heads);
-  const int n_items = n_seqs * heads;
+  const int n_items = n_tiles * heads;
   const int grid = n_items < num_sms ? n_items : num_sms;
   if (split) {
+    constexpr int SM = AtqCfg<true>::SMEM;
     cudaFuncSetAttribute(attention_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         ATP_SMEM);
-    attention_tc_kernel<true><<<grid, ATP_THREADS, ATP_SMEM, st>>>(
-        *mh, *ml, cu, seqs, n_items, heads, d, scale, fmt, ch, cl, ldc, ovf);
+                         SM);
+    attention_tc_kernel<true><<<grid, ATQ_THREADS, SM, st>>>(
+        *mh, *ml, tiles, rng, n_items, heads, d, scale, fmt, ch, cl, ldc);
   } else {
+    constexpr int SM = AtqCfg<false>::SMEM;
     cudaFuncSetAttribute(attention_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         ATP_SMEM);
-    attention_tc_kernel<false><<<grid, ATP_THREADS, ATP_SMEM, st>>>(
-        *mh, *mh, cu, seqs, n_items, heads, d, scale, fmt, ch, cl, ldc, ovf);
+                         SM);
+    attention_tc_kernel<false><<<grid, ATQ_THREADS, SM, st>>>(
+        *mh, *mh, tiles, rng, n_items, heads, d, scale, fmt, ch, cl, ldc);
   }
   return cudaGetLastError();
 }

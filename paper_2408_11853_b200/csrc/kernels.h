@@ -5,6 +5,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <vector>
+
 namespace mfg {
 
 cudaError_t launch_embed(const int32_t* ids, const int32_t* cu, int nseq, int V, int d,
@@ -19,12 +21,20 @@ cudaError_t launch_attention(const uint16_t* qh, const uint16_t* ql, int ldq, in
                              const int32_t* cu,
                              const int2* work, int n_work, uint16_t* ch, uint16_t* cl,
                              int ldc, int fmt, int* ovf, cudaStream_t st);
-// Persistent tcgen05 attention over (listed sequence, head) items; L <= 128,
-// d_head == 64. Maps: Q|K|V hi/lo [T][ldq] with box {64 cols, 16 rows}.
+// Persistent tcgen05 attention over (tile, head) items; tiles pack whole
+// sequences of <= 128 tokens into <= 128 consecutive rows (att_plan_tiles),
+// d_head == 64. Maps: Q|K|V hi/lo [T][ldq] with box {64 cols, 128 rows};
+// rng[t] = [start, end) of token t's sequence (launch_token_ranges).
 cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml, bool split,
-                                const int32_t* cu, const int32_t* seqs, int n_seqs, int heads,
-                                int d, int fmt, uint16_t* ch, uint16_t* cl, int ldc, int* ovf,
+                                const int2* tiles, int n_tiles, const int2* rng, int heads, int d,
+                                int fmt, uint16_t* ch, uint16_t* cl, int ldc, int* ovf,
                                 int num_sms, cudaStream_t st);
+cudaError_t att_set_trace(long long* dev_buf);  // diagnostics: [4][64][8] clock64 or null
+cudaError_t launch_token_ranges(const int32_t* cu, int nseq, int2* rng, cudaStream_t st);
+// Host: sequences of <= 128 tokens (when tc_ok) -> packed tiles {t0, rows};
+// the rest -> SIMT work items {seq, q0} (64-query blocks).
+void att_plan_tiles(const int32_t* cu, int nseq, bool tc_ok, std::vector<int2>& tiles,
+                    std::vector<int2>& work);
 cudaError_t launch_features(const float* x, int ld, int d, int kind, const int32_t* cu, int n,
                             uint16_t* fh, uint16_t* fl, int ldf, int fmt, int* ovf,
                             cudaStream_t st);

@@ -4,6 +4,7 @@
 // uploaded once, matrices transposed to K-major and split into bf16 hi/lo pairs
 // (fp32-parity) or rounded to bf16 (bf16 mode); a batch of records is scored as
 // one token-packed stream per device chunk.
+#include <algorithm>
 #include <cerrno>
 #include <chrono>
 #include <cmath>
@@ -93,9 +94,10 @@ struct mfg_ctx {
   int cap_records = 0;
   float *x32 = nullptr, *y32 = nullptr;
   Act xa, ca, ha, fa, qa;          // qa: Q|K|V pieces [T][qkv_ld]
-  CUtensorMap qmh16{}, qml16{};     // Q|K|V maps with 16-row boxes (attention)
   bool att_tc = false;              // tcgen05 attention usable (d_head == 64)
-  int32_t *d_short = nullptr, *h_short = nullptr;
+  int2 *d_tiles = nullptr, *h_tiles = nullptr;  // packed attention tiles {t0, rows}
+  int2* d_rng = nullptr;            // per token: [start, end) of its sequence
+  std::vector<int2> v_tiles, v_work;
   std::vector<Act> ga;  // head hidden-stage outputs
   float* hout = nullptr;
   float* dscores = nullptr;
@@ -324,13 +326,6 @@ struct mfg_ctx {
     x32 = dalloc<float>((size_t)cap_tokens * dp);
     y32 = dalloc<float>((size_t)cap_tokens * dp);
     make_act(qa, cap_tokens, qkv_ld);
-    {
-      char err[256];
-      if (!make_tmap_u16(&qmh16, qa.hi, qa.rows, qa.ld, qa.ld, 16, err, sizeof err))
-        throw Fail{MFG_ERR_RUNTIME, err};
-      if (split && !make_tmap_u16(&qml16, qa.lo, qa.rows, qa.ld, qa.ld, 16, err, sizeof err))
-        throw Fail{MFG_ERR_RUNTIME, err};
-    }
     att_tc = (d / H == 64) && (d % 64 == 0);
     make_act(xa, cap_tokens, dp);
     make_act(ca, cap_tokens, dp);
@@ -342,8 +337,9 @@ struct mfg_ctx {
     dscores = dalloc<float>(cap_records);
     d_ids = dalloc<int32_t>(cap_tokens);
     d_cu = dalloc<int32_t>((size_t)cap_records * n_roles + 1);
-    d_short = dalloc<int32_t>((size_t)cap_records * n_roles);
-    CK(cudaMallocHost(&h_short, (size_t)cap_records * n_roles * 4));
+    d_tiles = dalloc<int2>((size_t)cap_records * n_roles);
+    CK(cudaMallocHost(&h_tiles, (size_t)cap_records * n_roles * sizeof(int2)));
+    d_rng = dalloc<int2>(cap_tokens);
     work_cap = cap_tokens / 1 + (int64_t)cap_records * n_roles;
     d_work = dalloc<int2>(work_cap);
     CK(cudaMallocHost(&h_ids, cap_tokens * 4));
@@ -393,12 +389,15 @@ struct mfg_ctx {
   // One device chunk: m records, T tokens, role-major packing in h_* staging.
   // One device chunk: m records, T tokens; ids already in d_ids (role-major),
   // cu / work items in the pinned h_* staging. Scores land in dscores[0..m).
-  void forward_chunk(int m, int64_t T, int64_t n_work, int n_short, double sum_l2) {
+  void forward_chunk(int m, int64_t T, int64_t n_work, int n_tiles, double sum_l2) {
     const int nseq = m * n_roles;
     CK(cudaMemcpyAsync(d_cu, h_cu, (nseq + 1) * 4, cudaMemcpyHostToDevice, st));
-    if (n_short > 0)
-      CK(cudaMemcpyAsync(d_short, h_short, n_short * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_work, h_work, n_work * sizeof(int2), cudaMemcpyHostToDevice, st));
+    if (n_tiles > 0) {
+      CK(cudaMemcpyAsync(d_tiles, h_tiles, n_tiles * sizeof(int2), cudaMemcpyHostToDevice, st));
+      CK(launch_token_ranges(d_cu, nseq, d_rng, st));
+    }
+    if (n_work > 0)
+      CK(cudaMemcpyAsync(d_work, h_work, n_work * sizeof(int2), cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(d_ovf, 0, sizeof(int), st));
     const int Ti = (int)T;
     {
@@ -413,14 +412,14 @@ struct mfg_ctx {
       {
         const double bytes = (double)T * d * 4 * (split ? 4 : 2);
         int e = ev_begin();
-        if (n_short > 0)
-          CK(launch_attention_tc(&qmh16, split ? &qml16 : &qmh16, split, d_cu, d_short, n_short,
+        if (n_tiles > 0)
+          CK(launch_attention_tc(&qa.mh, split ? &qa.ml : &qa.mh, split, d_tiles, n_tiles, d_rng,
                                  H, d, fmt, ca.hi, ca.lo, ca.ld, d_ovf, num_sms, st));
         if (n_work > 0)
           CK(launch_attention(qa.hi, qa.lo, qa.ld, d, H, d_cu, d_work, (int)n_work, ca.hi, ca.lo,
                               ca.ld, fmt, d_ovf, st));
         ev_end(e, C_ATT, 4.0 * sum_l2 * d, bytes);
-        if (n_short > 0 && n_work > 0) stats.kernel_launches += 1;
+        if (n_tiles > 0 && n_work > 0) stats.kernel_launches += 1;
       }
       gemm(ca, L.o, Ti, EPI_F32_RES, C_O, x32, dp, y32, dp, nullptr);
       if (!pre_norm) {
@@ -514,8 +513,7 @@ struct mfg_ctx {
       if (r1 == r0) throw Fail{MFG_ERR_USAGE, "record exceeds device chunk capacity"};
       const int m = r1 - r0;
       // role-major chunk: cu / work items on the host, ids staged per role
-      int64_t at = 0, nw = 0;
-      int ns = 0;
+      int64_t at = 0;
       double sum_l2 = 0;
       h_cu[0] = 0;
       for (int k = 0; k < n_roles; ++k) {
@@ -528,20 +526,16 @@ struct mfg_ctx {
         for (int64_t s = s0; s < s1; ++s) {
           const int64_t L = cu[s + 1] - cu[s];
           const int ls = (int)(k * m + (s - s0));
-          if (att_tc && L <= 128)
-            h_short[ns++] = ls;
-          else
-            for (int64_t q = 0; q < L; q += 64) h_work[nw++] = make_int2(ls, (int)q);
           h_cu[ls + 1] = (int32_t)(at + (cu[s + 1] - cu[s0]));
           sum_l2 += (double)L * L;
         }
         at += len;
       }
+      att_plan_tiles(h_cu, m * n_roles, att_tc, v_tiles, v_work);
+      std::copy(v_tiles.begin(), v_tiles.end(), h_tiles);
+      std::copy(v_work.begin(), v_work.end(), h_work);
       if (!device_io) CK(cudaMemcpyAsync(d_ids, h_ids, T * 4, cudaMemcpyHostToDevice, st));
-      if (nw > 0)
-        CK(cudaMemcpyAsync(d_work, h_work, nw * sizeof(int2), cudaMemcpyHostToDevice, st));
-      CK(cudaMemsetAsync(d_ovf, 0, sizeof(int), st));
-      forward_chunk(m, T, nw, ns, sum_l2);
+      forward_chunk(m, T, (int64_t)v_work.size(), (int)v_tiles.size(), sum_l2);
       if (device_io) {
         CK(cudaMemcpyAsync(out + r0, dscores, m * 4, cudaMemcpyDeviceToDevice, st));
         check_flag();
@@ -571,7 +565,7 @@ struct mfg_ctx {
     if (h_cu) cudaFreeHost(h_cu);
     if (h_work) cudaFreeHost(h_work);
     if (h_scores) cudaFreeHost(h_scores);
-    if (h_short) cudaFreeHost(h_short);
+    if (h_tiles) cudaFreeHost(h_tiles);
     if (h_ovf) cudaFreeHost(h_ovf);
     for (auto e : pev) cudaEventDestroy(e);
     if (ev0) cudaEventDestroy(ev0);
@@ -856,33 +850,28 @@ extern "C" int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* c
     int32_t* dcu = s.alloc<int32_t>(n_seq + 1);
     CK(cudaMemcpy(dcu, cu, (n_seq + 1) * 4, cudaMemcpyHostToDevice));
     const bool tc_ok = use_tc && (d / n_heads == 64) && (d % 64 == 0);
-    std::vector<int2> work;
-    std::vector<int32_t> shorts;
-    for (int i = 0; i < n_seq; ++i) {
-      const int L = cu[i + 1] - cu[i];
-      if (tc_ok && L <= 128)
-        shorts.push_back(i);
-      else
-        for (int q = 0; q < L; q += 64) work.push_back(make_int2(i, q));
-    }
+    std::vector<int2> work, tiles;
+    att_plan_tiles(cu, n_seq, tc_ok, tiles, work);
     int2* dw = s.alloc<int2>(work.size());
     if (!work.empty())
       CK(cudaMemcpy(dw, work.data(), work.size() * sizeof(int2), cudaMemcpyHostToDevice));
-    int32_t* dsh = s.alloc<int32_t>(shorts.size());
-    if (!shorts.empty())
-      CK(cudaMemcpy(dsh, shorts.data(), shorts.size() * 4, cudaMemcpyHostToDevice));
+    int2* dt = s.alloc<int2>(tiles.size());
+    if (!tiles.empty())
+      CK(cudaMemcpy(dt, tiles.data(), tiles.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    int2* drng = s.alloc<int2>(T);
+    CK(launch_token_ranges(dcu, n_seq, drng, 0));
     auto* ch = s.alloc<uint16_t>((size_t)T * ldc);
     auto* cl = split ? s.alloc<uint16_t>((size_t)T * ldc) : nullptr;
-    if (!shorts.empty()) {
-      CUtensorMap m16h, m16l;
-      if (!make_tmap_u16(&m16h, qh, Tp, ldq, ldq, 16, err, sizeof err))
+    if (!tiles.empty()) {
+      CUtensorMap mh, ml;
+      if (!make_tmap_u16(&mh, qh, Tp, ldq, ldq, 128, err, sizeof err))
         throw Fail{MFG_ERR_RUNTIME, err};
-      if (split && !make_tmap_u16(&m16l, ql, Tp, ldq, ldq, 16, err, sizeof err))
+      if (split && !make_tmap_u16(&ml, ql, Tp, ldq, ldq, 128, err, sizeof err))
         throw Fail{MFG_ERR_RUNTIME, err};
       int sms = 148, dev = 0;
       CK(cudaGetDevice(&dev));
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      CK(launch_attention_tc(&m16h, split ? &m16l : &m16h, split, dcu, dsh, (int)shorts.size(),
+      CK(launch_attention_tc(&mh, split ? &ml : &mh, split, dt, (int)tiles.size(), drng,
                              n_heads, d, fmt, ch, cl, ldc, nullptr, sms, 0));
     }
     if (!work.empty())
@@ -893,6 +882,24 @@ extern "C" int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* c
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(ctx_out, o, (size_t)T * d * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+// Diagnostics: route the next attention launches' per-item clock64 trace to a
+// device buffer (enable = 1), or copy it to host_out[4*64*8] and stop (enable = 0).
+extern "C" int mfgt_att_trace(int32_t enable, long long* host_out) {
+  static long long* buf = nullptr;
+  return guarded([&] {
+    const size_t n = 4 * 64 * 8;
+    if (enable) {
+      if (!buf) CK(cudaMalloc(&buf, n * sizeof(long long)));
+      CK(cudaMemset(buf, 0, n * sizeof(long long)));
+      CK(att_set_trace(buf));
+    } else {
+      CK(cudaDeviceSynchronize());
+      CK(att_set_trace(nullptr));
+      if (buf && host_out) CK(cudaMemcpy(host_out, buf, n * sizeof(long long), cudaMemcpyDeviceToHost));
+    }
   });
 }
 

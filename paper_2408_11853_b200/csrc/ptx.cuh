@@ -33,11 +33,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
+#ifdef MFG_NO_SUSPEND_HINT
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+#else
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+      : "memory");
+#endif
   return ok != 0;
 }
 // Non-blocking probe of a phase (for event-loop style issuers).
@@ -53,10 +61,13 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 // Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
+// try_wait carries a suspend-time hint, so a waiting warp sleeps in hardware
+// until the phase flips instead of spinning on issue slots its neighbours need.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t spins = 0;
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
-    if (++spins > (1u << 26)) __trap();
+    if (clock64() - t0 > (1ll << 33)) __trap();  // ~4 s at 2 GHz
   }
 }
 
@@ -175,6 +186,30 @@ __device__ __forceinline__ bool split16(float v, int fmt, uint16_t& hi, uint16_t
   hi = __bfloat16_as_ushort(h);
   lo = __bfloat16_as_ushort(__float2bfloat16_rn(v - __bfloat162float(h)));
   return true;
+}
+// Two values -> packed (hi, lo) 16-bit pairs (element a in the low half), no
+// range check: for values already known to be inside the fp16 range (softmax
+// weights in [0, 1], convex combinations of range-checked values).
+__device__ __forceinline__ void split2(float a, float b, int fmt, uint32_t& hi, uint32_t& lo) {
+  if (fmt == FMT_F16) {
+    const __half2 h = __floats2half2_rn(a, b);
+    const float2 f = __half22float2(h);
+    const __half2 l = __floats2half2_rn(a - f.x, b - f.y);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
+  } else {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    const float2 f = __bfloat1622float2(h);
+    const __nv_bfloat162 l = __floats2bfloat162_rn(a - f.x, b - f.y);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
+  }
+}
+// 2^x via MUFU.EX2 (max relative error ~2^-22, far below the operand split).
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 // Store v as hi (and lo, when non-null) at index i; flag fp16 overflow.
 __device__ __forceinline__ void store_split(uint16_t* __restrict__ hi, uint16_t* __restrict__ lo,

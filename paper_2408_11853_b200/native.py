@@ -116,6 +116,8 @@ def gpu():
             lib.mfgt_attention.restype = C.c_int
             lib.mfgt_layernorm.argtypes = [i32, i32, f32p, f32p, f32p, f32p]
             lib.mfgt_layernorm.restype = C.c_int
+            lib.mfgt_att_trace.argtypes = [i32, C.POINTER(C.c_longlong)]
+            lib.mfgt_att_trace.restype = C.c_int
             _gpu = lib
     return _gpu
 
