@@ -1,6 +1,7 @@
 // Host side of the tcgen05 GEMM: tensor-map encoding (driver entry point, no
 // libcuda link dependency) and the template dispatch.
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm_tc.cuh"
@@ -50,6 +51,18 @@ bool make_tmap_u16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t co
   return true;
 }
 
+// BN = 256 weights run on the CTA-pair kernel (tcgen05 cta_group::2);
+// MFG_GEMM_SINGLE=1 in the environment forces the single-CTA kernel (A/B runs).
+bool gemm_uses_pair(int bn) {
+  static const bool single = [] {
+    const char* e = getenv("MFG_GEMM_SINGLE");
+    return e && e[0] == '1';
+  }();
+  return bn == 256 && !single;
+}
+
+int gemm_b_box_rows(int bn) { return gemm_uses_pair(bn) ? 128 : bn; }
+
 int gemm_pick_bn(int n_pad) {
   if (n_pad % 256 == 0) return 256;
   if (n_pad % 128 == 0) return 128;
@@ -72,6 +85,36 @@ static cudaError_t run(const CUtensorMap* ah, const CUtensorMap* al, const CUten
   return cudaGetLastError();
 }
 
+template <bool SPLIT, int EPI>
+static cudaError_t run2(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* bh,
+                        const CUtensorMap* bl, const GemmArgs& a, int num_sms, cudaStream_t st) {
+  using C = Gemm2Cfg<SPLIT>;
+  auto kern = gemm2_tc_kernel<SPLIT, EPI>;
+  cudaError_t e =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const int tiles = ((a.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * (a.N / 256);
+  if (tiles <= 0) return cudaSuccess;
+  const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  kern<<<2 * pairs, GEMM_THREADS, C::SMEM_BYTES, st>>>(*ah, SPLIT ? *al : *ah, *bh,
+                                                       SPLIT ? *bl : *bh, a);
+  return cudaGetLastError();
+}
+
+template <bool SPLIT>
+static cudaError_t run2_epi(int epi, const CUtensorMap* ah, const CUtensorMap* al,
+                            const CUtensorMap* bh, const CUtensorMap* bl, const GemmArgs& a,
+                            int num_sms, cudaStream_t st) {
+  switch (epi) {
+    case EPI_F32: return run2<SPLIT, EPI_F32>(ah, al, bh, bl, a, num_sms, st);
+    case EPI_F32_RES: return run2<SPLIT, EPI_F32_RES>(ah, al, bh, bl, a, num_sms, st);
+    case EPI_GELU_SPLIT: return run2<SPLIT, EPI_GELU_SPLIT>(ah, al, bh, bl, a, num_sms, st);
+    case EPI_TANH_SPLIT: return run2<SPLIT, EPI_TANH_SPLIT>(ah, al, bh, bl, a, num_sms, st);
+    case EPI_SPLIT: return run2<SPLIT, EPI_SPLIT>(ah, al, bh, bl, a, num_sms, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
 template <int BN, bool SPLIT>
 static cudaError_t run_epi(int epi, const CUtensorMap* ah, const CUtensorMap* al,
                            const CUtensorMap* bh, const CUtensorMap* bl, const GemmArgs& a,
@@ -91,6 +134,9 @@ cudaError_t launch_gemm(const CUtensorMap* ah, const CUtensorMap* al, const CUte
                         int num_sms, cudaStream_t st) {
   if (a.K % GEMM_BK != 0 || a.N % bn != 0) return cudaErrorInvalidValue;
   const bool split = nsplit == 2;
+  if (gemm_uses_pair(bn))
+    return split ? run2_epi<true>(epi, ah, al, bh, bl, a, num_sms, st)
+                 : run2_epi<false>(epi, ah, al, bh, bl, a, num_sms, st);
   if (split) {
     if (bn == 256) return run_epi<256, true>(epi, ah, al, bh, bl, a, num_sms, st);
     if (bn == 128) return run_epi<128, true>(epi, ah, al, bh, bl, a, num_sms, st);

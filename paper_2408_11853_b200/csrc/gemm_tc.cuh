@@ -73,6 +73,70 @@ struct GemmCfg {
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
 };
 
+// One accumulator tile's epilogue for one warp: TMEM lanes = tile rows
+// row0..row0+rows-1 (this warp's quarter), every other 32-column chunk starting
+// at `half`*32; each chunk transposed through `buf` so global traffic is float4
+// per lane, 4 full 128-byte row segments per warp instruction.
+template <int BN, int EPI>
+__device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, int row0, int rows,
+                                         int n0, int half, float* buf, int lane) {
+  const int cg = lane & 7;       // transposed phase: 4 columns 4*cg..4*cg+3
+  const int rs = lane >> 3;      // row sub-index 0..3
+#pragma unroll 1
+  for (int c = half * 32; c < BN; c += 64) {
+    const int col = n0 + c + 4 * cg;
+    // prefetch this chunk's residual (8 x float4 per lane) before touching TMEM
+    float4 res[8];
+    if (EPI == EPI_F32_RES) {
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int r = it * 4 + rs;
+        res[it] = r < rows ? *reinterpret_cast<const float4*>(
+                                 args.residual + (size_t)(row0 + r) * args.ldr + col)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    float v[32];
+    tmem_ld_32x32(tacc + c, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = v[i];
+    __syncwarp();
+    const float4 b = *reinterpret_cast<const float4*>(args.bias + col);
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int r = it * 4 + rs;
+      if (r < rows) {
+        const float* src = buf + r * 33 + 4 * cg;
+        float x[4] = {src[0] + b.x, src[1] + b.y, src[2] + b.z, src[3] + b.w};
+        const size_t o = (size_t)(row0 + r);
+        if (EPI == EPI_F32 || EPI == EPI_F32_RES) {
+          if (EPI == EPI_F32_RES) {
+            x[0] += res[it].x; x[1] += res[it].y; x[2] += res[it].z; x[3] += res[it].w;
+          }
+          *reinterpret_cast<float4*>(args.out_f32 + o * args.ldo + col) =
+              make_float4(x[0], x[1], x[2], x[3]);
+        } else {
+          uint16_t h[4], l[4];
+          bool ok = true;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float y = (EPI == EPI_GELU_SPLIT) ? gelu_tanh(x[j])
+                            : (EPI == EPI_TANH_SPLIT) ? tanhf(x[j]) : x[j];
+            ok &= split16(y, args.fmt, h[j], l[j]);
+          }
+          if (!ok && args.ovf) atomicOr(args.ovf, 1);
+          *reinterpret_cast<uint2*>(args.out_hi + o * args.ldh + col) =
+              make_uint2(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16));
+          if (args.out_lo)
+            *reinterpret_cast<uint2*>(args.out_lo + o * args.ldh + col) =
+                make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 template <int BN, bool SPLIT, int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapAh,
@@ -195,8 +259,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int q = warp & 3;        // TMEM lane quarter == 32-row block of the tile
     const int half = ew >> 2;      // which alternate 32-column chunks this warp owns
     float* buf = epi_buf + ew * 32 * 33;
-    const int cg = lane & 7;       // transposed phase: 4 columns 4*cg..4*cg+3
-    const int rs = lane >> 3;      // row sub-index 0..3
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -206,59 +268,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int rows = min(32, args.M - row0);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-#pragma unroll 1
-      for (int c = half * 32; c < BN; c += 64) {
-        const int col = n0 + c + 4 * cg;
-        // prefetch this chunk's residual (8 x float4 per lane) before touching TMEM
-        float4 res[8];
-        if (EPI == EPI_F32_RES) {
-#pragma unroll
-          for (int it = 0; it < 8; ++it) {
-            const int r = it * 4 + rs;
-            res[it] = r < rows ? *reinterpret_cast<const float4*>(
-                                     args.residual + (size_t)(row0 + r) * args.ldr + col)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-        float v[32];
-        tmem_ld_32x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = v[i];
-        __syncwarp();
-        const float4 b = *reinterpret_cast<const float4*>(args.bias + col);
-#pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int r = it * 4 + rs;
-          if (r < rows) {
-            const float* src = buf + r * 33 + 4 * cg;
-            float x[4] = {src[0] + b.x, src[1] + b.y, src[2] + b.z, src[3] + b.w};
-            const size_t o = (size_t)(row0 + r);
-            if (EPI == EPI_F32 || EPI == EPI_F32_RES) {
-              if (EPI == EPI_F32_RES) {
-                x[0] += res[it].x; x[1] += res[it].y; x[2] += res[it].z; x[3] += res[it].w;
-              }
-              *reinterpret_cast<float4*>(args.out_f32 + o * args.ldo + col) =
-                  make_float4(x[0], x[1], x[2], x[3]);
-            } else {
-              uint16_t h[4], l[4];
-              bool ok = true;
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float y = (EPI == EPI_GELU_SPLIT) ? gelu_tanh(x[j])
-                                : (EPI == EPI_TANH_SPLIT) ? tanhf(x[j]) : x[j];
-                ok &= split16(y, args.fmt, h[j], l[j]);
-              }
-              if (!ok && args.ovf) atomicOr(args.ovf, 1);
-              *reinterpret_cast<uint2*>(args.out_hi + o * args.ldh + col) =
-                  make_uint2(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16));
-              if (args.out_lo)
-                *reinterpret_cast<uint2*>(args.out_lo + o * args.ldh + col) =
-                    make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
-            }
-          }
-        }
-        __syncwarp();
-      }
+      epi_tile<BN, EPI>(args, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, row0, rows, n0,
+                        half, buf, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -272,6 +283,192 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------------
+// CTA-pair variant (cluster of 2, tcgen05 cta_group::2), BN = 256: one tile is
+// 256 rows x 256 columns; CTA rank r loads A rows m0+128r..+127 and B (weight)
+// rows n0+128r..+127 into its own shared memory, the leader (rank 0) issues
+// M=256 x N=256 x K=16 MMAs that read both CTAs' halves, and each CTA's
+// accumulator (its 128 rows x 256 columns) lands in its own TMEM. Per CTA a
+// k-block stage is A 16 KB + B 16 KB per piece instead of 16 + 32 KB, so three
+// stages fit and each CTA pulls half the weight bytes per FLOP from L2.
+// Barriers: full[s] lives in the leader (both CTAs' TMA bytes complete on it);
+// empty[s] / tfull[a] are signalled in both CTAs by a multicast commit;
+// tempty[a] lives in the leader and counts both CTAs' epilogue warps.
+template <bool SPLIT>
+struct Gemm2Cfg {
+  static constexpr int NOPS = SPLIT ? 2 : 1;
+  static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;  // this CTA's 128 rows
+  static constexpr int B_BYTES = 128 * GEMM_BK * 2;      // this CTA's half of BN = 256
+  static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
+  static constexpr int STAGES_FIT =
+      (GEMM_SMEM_LIMIT - 1024 - GEMM_EPI_BYTES - GEMM_BAR_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + GEMM_EPI_BYTES + GEMM_BAR_BYTES;
+  static_assert(STAGES >= 2, "pipeline needs at least two stages");
+};
+
+template <bool SPLIT, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    gemm2_tc_kernel(const __grid_constant__ CUtensorMap mapAh,
+                    const __grid_constant__ CUtensorMap mapAl,
+                    const __grid_constant__ CUtensorMap mapBh,
+                    const __grid_constant__ CUtensorMap mapBl, const GemmArgs args) {
+  using C = Gemm2Cfg<SPLIT>;
+  constexpr int BN = 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  float* epi_buf = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + GEMM_EPI_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapAh);
+    tma_prefetch(&mapBh);
+    if (SPLIT) {
+      tma_prefetch(&mapAl);
+      tma_prefetch(&mapBl);
+    }
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * GEMM_EPI_WARPS);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_m = (args.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM);
+  const int num_n = args.N / BN;
+  const int tiles = num_m * num_n;
+  const int kblocks = args.K / GEMM_BK;
+
+  auto stage_ptr = [&](int s, int which) -> uint8_t* {
+    // which: 0 A_hi, 1 A_lo, 2 B_hi, 3 B_lo
+    uint8_t* base = smem + s * C::STAGE_BYTES;
+    if (which < 2) return base + which * C::A_BYTES;
+    return base + C::NOPS * C::A_BYTES + (which - 2) * C::B_BYTES;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = pair; tile < tiles; tile += npairs) {
+        const int m0 = (tile / num_n) * 2 * GEMM_BM + rank * GEMM_BM;
+        const int n0 = (tile % num_n) * BN + rank * 128;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+          const int k0 = kb * GEMM_BK;
+          tma_load_2d_pair(stage_ptr(stage, 0), &mapAh, &full[stage], k0, m0);
+          tma_load_2d_pair(stage_ptr(stage, 2), &mapBh, &full[stage], k0, n0);
+          if (SPLIT) {
+            tma_load_2d_pair(stage_ptr(stage, 1), &mapAl, &full[stage], k0, m0);
+            tma_load_2d_pair(stage_ptr(stage, 3), &mapBl, &full[stage], k0, n0);
+          }
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      // drain: the leader's last multicast commits must land before this CTA exits
+      for (int i = 0; i < C::STAGES; ++i) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc = idesc_f16kind(2 * GEMM_BM, BN, (uint32_t)args.fmt);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = pair; tile < tiles; tile += npairs) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ah = umma_desc_sw128(stage_ptr(stage, 0));
+          const uint64_t bh = umma_desc_sw128(stage_ptr(stage, 2));
+          const uint64_t al = SPLIT ? umma_desc_sw128(stage_ptr(stage, 1)) : 0;
+          const uint64_t bl = SPLIT ? umma_desc_sw128(stage_ptr(stage, 3)) : 0;
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k) {
+            const uint64_t adv = (uint64_t)(k * 32) >> 4;  // 16 elements along K
+            tc_mma_pair(d, ah + adv, bh + adv, idesc, (kb | k) != 0);
+            if (SPLIT) {
+              tc_mma_pair(d, al + adv, bh + adv, idesc, 1);
+              tc_mma_pair(d, ah + adv, bl + adv, idesc, 1);
+            }
+          }
+          tc_commit_pair(&empty[stage], 3);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit_pair(&tfull[acc], 3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;       // 0..7
+    const int q = warp & 3;        // TMEM lane quarter == 32-row block of this CTA's half tile
+    const int half = ew >> 2;      // which alternate 32-column chunks this warp owns
+    float* buf = epi_buf + ew * 32 * 33;
+    const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = pair; tile < tiles; tile += npairs) {
+      const int m0 = (tile / num_n) * 2 * GEMM_BM + rank * GEMM_BM;
+      const int n0 = (tile % num_n) * BN;
+      const int row0 = m0 + q * 32;
+      const int rows = min(32, args.M - row0);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      if (rows > 0)
+        epi_tile<BN, EPI>(args, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, row0, rows, n0,
+                          half, buf, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem_base);
   }
 }
 

@@ -49,6 +49,10 @@ bool make_tmap_u16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t co
                     uint64_t ld_elems, uint32_t box_rows, char* err, size_t errcap);
 // Largest supported N tile dividing n_pad (n_pad % 64 == 0).
 int gemm_pick_bn(int n_pad);
+// Whether N tile `bn` runs on the CTA-pair kernel, and the weight tensor-map box
+// rows that kernel expects (each CTA of a pair loads half of the N tile).
+bool gemm_uses_pair(int bn);
+int gemm_b_box_rows(int bn);
 // nsplit: 1 = one MMA per k-step (hi only), 2 = hi/lo pieces, 3 MMAs per k-step.
 cudaError_t launch_gemm(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* bh,
                         const CUtensorMap* bl, int bn, int nsplit, int epi, const GemmArgs& a,

@@ -209,9 +209,10 @@ struct mfg_ctx {
       CK(cudaMemcpy(w.bias + off, src, b->numel() * 4, cudaMemcpyHostToDevice));
       off += (int)b->numel();
     }
-    if (!make_tmap_u16(&w.mh, w.hi, w.Npad, w.Kpad, w.Kpad, w.bn, err, sizeof err))
+    if (!make_tmap_u16(&w.mh, w.hi, w.Npad, w.Kpad, w.Kpad, gemm_b_box_rows(w.bn), err, sizeof err))
       throw Fail{MFG_ERR_RUNTIME, err};
-    if (split && !make_tmap_u16(&w.ml, w.lo, w.Npad, w.Kpad, w.Kpad, w.bn, err, sizeof err))
+    if (split && !make_tmap_u16(&w.ml, w.lo, w.Npad, w.Kpad, w.Kpad, gemm_b_box_rows(w.bn), err,
+                                sizeof err))
       throw Fail{MFG_ERR_RUNTIME, err};
   }
 
@@ -797,10 +798,10 @@ extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, i
     auto* ol = split ? s.alloc<uint16_t>((size_t)M * Np) : nullptr;
     CUtensorMap mah, mal, mwh, mwl;
     if (!make_tmap_u16(&mah, ah, Mp, Kp, Kp, GEMM_BM, err, sizeof err) ||
-        !make_tmap_u16(&mwh, wh, Np, Kp, Kp, bn, err, sizeof err))
+        !make_tmap_u16(&mwh, wh, Np, Kp, Kp, gemm_b_box_rows(bn), err, sizeof err))
       throw Fail{MFG_ERR_RUNTIME, err};
     if (split && (!make_tmap_u16(&mal, al, Mp, Kp, Kp, GEMM_BM, err, sizeof err) ||
-                  !make_tmap_u16(&mwl, wl, Np, Kp, Kp, bn, err, sizeof err)))
+                  !make_tmap_u16(&mwl, wl, Np, Kp, Kp, gemm_b_box_rows(bn), err, sizeof err)))
       throw Fail{MFG_ERR_RUNTIME, err};
     GemmArgs g{};
     g.M = M;
