@@ -193,20 +193,33 @@ def cpu_baseline(cfg, n_records, return_scores=False):
     return (out, lines, ref_scores) if return_scores else out
 
 
-def parity_report(path, vocab_path, lines, ref, device):
+def parity_report(path, vocab_path, lines, ref, device, cfg_id):
     """Same records through the device path at every precision vs the fp32
-    oracle (the reference algorithm): max/mean |delta| and Pearson."""
+    oracle (the reference algorithm): max/mean |delta| and Pearson; the fp16
+    mode also against the oracle's fp16 mode (the reference's binary16 path)."""
     import paper_2408_11853_b200 as mf
+    from oracle import evaluate as oe
+    from oracle.encoder import OracleModel
+
     ref = np.asarray(ref, dtype=np.float64)
     out = {"n_records": len(lines), "tolerance": 1e-3, "reference": "oracle fp32 (numpy port)"}
-    for prec in ("fp32", "bf16x3", "bf16"):
+
+    def stats(got, want):
+        d = np.abs(got - want)
+        pear = float(np.corrcoef(got, want)[0, 1]) if len(got) > 2 and want.std() > 0 else None
+        return {"max_abs": float(d.max()), "mean_abs": float(d.mean()), "pearson": pear}
+
+    for prec in ("fp32", "bf16x3", "bf16", "fp16"):
         cfg = mf.EvaluatorConfig(model=path, vocab=vocab_path, quiet=True, validate=False,
                                  device=device, precision=prec)
         with mf.Evaluator(cfg) as ev:
             got = np.asarray(ev.evaluate_lines(lines).segment_scores, dtype=np.float64)
-        d = np.abs(got - ref)
-        pear = float(np.corrcoef(got, ref)[0, 1]) if len(got) > 2 and ref.std() > 0 else None
-        out[prec] = {"max_abs": float(d.max()), "mean_abs": float(d.mean()), "pearson": pear}
+        out[prec] = stats(got, ref)
+        if prec == "fp16":
+            model32, vocab = oracle_model(cfg_id)
+            m16 = OracleModel(model32.m, {k: v for k, v in model32.w.items()}, mode="fp16")
+            want16, _ = oe.score_lines(m16, vocab, lines)
+            out["fp16"]["vs_reference_fp16_mode"] = stats(got, np.asarray(want16, np.float64))
     out["fp32_within_tolerance"] = out["fp32"]["max_abs"] <= 1e-3
     return out
 
@@ -306,6 +319,29 @@ def run_ours(args, rank, world, local_rank):
     stats = model.stats()
     model.set_stream(0)
     model.close()
+
+    # ---------------- the other device precisions, same inputs (reported beside value)
+    others = {}
+    if world == 1 and not args.no_other_precisions:
+        for prec in ("fp16", "bf16", "fp32"):
+            if prec == args.precision:
+                continue
+            m2 = mf.GpuScoringModel(path, device=local_rank, precision=prec)
+            m2.set_stream(stream.cuda_stream)
+            for s in range(min(args.warmup, 2)):
+                m2.score_device(steps[s][0].data_ptr(), steps[s][1], R, out.data_ptr())
+            k2 = min(args.steps, 6)
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            for s in range(args.warmup, args.warmup + k2):
+                m2.score_device(steps[s][0].data_ptr(), steps[s][1], R, out.data_ptr())
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            ms2 = ev0.elapsed_time(ev1)
+            m2.set_stream(0)
+            m2.close()
+            others[prec] = {"value": R * k2 / (ms2 / 1000.0), "unit": UNIT, "steps": k2,
+                            "ms_per_step": ms2 / k2}
     del steps
 
     # ---------------- end to end through the public API (e2e)
@@ -343,7 +379,7 @@ def run_ours(args, rank, world, local_rank):
     per_launch_ms = c["ms"] / max(1, c["launches"])
     achieved = (c["flops"] / max(1, c["launches"])) / (per_launch_ms / 1e3) / 1e12
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
-    mma_per_step = 1 if args.precision == "bf16" else 3
+    mma_per_step = 1 if args.precision in ("bf16", "fp16") else 3
     traffic, traffic_src = ncu_traffic()
     gemm_ms = sum(cls[k]["ms"] for k in gemm_names)
     gemm_flops = sum(cls[k]["flops"] for k in gemm_names)
@@ -374,7 +410,7 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
         "dtype": {"fp32": "fp16x3-split (fp32-parity)", "bf16x3": "bf16x3-split",
-                  "bf16": "bf16"}[args.precision],
+                  "bf16": "bf16", "fp16": "fp16 (reference binary16 mode)"}[args.precision],
         "data": ("synthetic (reference fixture generator, std-0.25 fixture weights)" if args.config == 1
                  else "synthetic (SURVEY §8d generator; random-init N(0,0.02) weights)"),
         "config": {"workload": f"config {args.config}: " + fx.CONFIG_NAMES[args.config],
@@ -388,12 +424,13 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": R * 4 + 4,
                 "path": "Evaluator.evaluate_lines (host TSV -> libmfhost -> libmfgpu -> scores)"},
         "gpu_launches": int(stats["kernel_launches"]),
+        "other_precisions": others,
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
         base, ref_lines, ref = cpu_baseline(args.config, args.cpu_records, return_scores=True)
         line["cpu_baseline"] = base
-        line["parity"] = parity_report(path, vocab_path, ref_lines, ref, local_rank)
+        line["parity"] = parity_report(path, vocab_path, ref_lines, ref, local_rank, args.config)
     print(json.dumps(line), flush=True)
 
 
@@ -404,10 +441,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16x3", "bf16"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16x3", "bf16", "fp16"])
     ap.add_argument("--records-per-step", type=int, default=RECORDS_PER_STEP)
     ap.add_argument("--cpu-records", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-precisions", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)

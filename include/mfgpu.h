@@ -38,6 +38,10 @@ extern "C" {
                              (~22 significant bits; |d| <= 1e-3 vs the fp32 reference) */
 #define MFG_PREC_BF16 1   /* one bf16 MMA per k-step, fp32 accumulate (reported separately) */
 #define MFG_PREC_BF16X3 2 /* bf16 hi/lo split, 3 MMAs: fp32 range, ~16 significant bits */
+#define MFG_PREC_FP16 3   /* the reference's fp16 mode (`encoder.py:105, 120-130`): binary16
+                             weights/activations, one fp16 MMA per k-step, fp32 accumulate,
+                             binary16 rounding after every matmul, bias add, LN, GELU,
+                             residual sum and head stage */
 
 typedef struct mfg_ctx mfg_ctx;
 

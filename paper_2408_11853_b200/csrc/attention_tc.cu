@@ -3,11 +3,15 @@
 // per-head loop of `pkg/src/metricforge/encoder.py:132-147` (+ masked_softmax 60-66).
 //
 // Tiles. The host packs whole sequences (each <= 128 tokens) greedily into tiles
-// of <= 128 consecutive rows of the token-packed stream (`att_plan_tiles`). A work
-// item is (tile, head); its S = Q·Kᵀ is block-diagonal: row r may only attend to
-// the keys of its own sequence, [rng[t].x, rng[t].y) (`token_ranges_kernel`),
-// every other key gets exactly 0 weight — which is the reference's per-sequence
-// masked softmax, so sequences never mix and padding never exists.
+// of 128 rows (`att_plan_tiles`, at most 4 sequences): sequence s of a tile sits
+// at tile row o_s, a multiple of 32, loaded by TMA in 32-row boxes. A work item
+// is (tile, head); its S = Q·Kᵀ is block-diagonal: a row attends only to the
+// keys of its own sequence, every other key gets exactly 0 weight — which is the
+// reference's per-sequence masked softmax, so sequences never mix. Because every
+// sequence starts on a 32-row boundary, its keys fall into the same 16-key MMA
+// k-steps and the same 32-key softmax chunks wherever it sits, and the other
+// sequences only add exact zeros: scores are bitwise independent of which
+// sequences share a tile (batch composition, chunking, GPU count).
 //
 // Per item:
 //   S = Q·Kᵀ      tcgen05.mma M=128 x N=round16(n) x K=64, Q/K from smem (TMA)
@@ -16,8 +20,11 @@
 //   O = P·V       tcgen05.mma M=128 x N=64 x K=round16(n), A = P from TMEM,
 //                 B = V (MN-major) from smem
 //   ctx = O / rowsum -> 16-bit hi/lo pieces (the O-projection's A operand)
-// With SPLIT every product is three MMAs (hi·hi + lo·hi + hi·lo) of fp16 (or
-// bf16) pieces, like the GEMMs (~22 significant bits with fp16).
+// MODE 3 (fp32 parity): every product is three MMAs (hi·hi + lo·hi + hi·lo) of
+// fp16 (or bf16) pieces, like the GEMMs (~22 significant bits with fp16).
+// MODE 2 (reference fp16 mode): Q, K, V are the binary16 values the reference
+// stores; S is one MMA (exact fp16 products, fp32 sums) and P = Ph + Pl keeps
+// the fp32 softmax weights: O = Ph·V + Pl·V. MODE 1 (bf16): one MMA each.
 //
 // Roles (576 threads, one CTA per SM, items round-robin):
 //   warp 0       TMA producer: Q|K ring (QK_ST stages) and V ring (V_ST stages)
@@ -45,8 +52,9 @@ namespace mfg {
 constexpr int ATQ_THREADS = 576;
 constexpr int ATQ_TILE = 128 * 128;  // 128 rows x 64 cols of 16-bit values (128B swizzle)
 
-template <bool SPLIT>
+template <int MODE>
 struct AtqCfg {
+  static constexpr bool SPLIT = MODE == 3;
   static constexpr int QK_BYTES = (SPLIT ? 4 : 2) * ATQ_TILE;  // Qh Kh (Ql Kl)
   static constexpr int V_BYTES = (SPLIT ? 2 : 1) * ATQ_TILE;   // Vh (Vl)
   static constexpr int QK_ST = SPLIT ? 2 : 3;
@@ -95,13 +103,26 @@ __device__ long long* g_att_trace = nullptr;
       g_att_trace[(blockIdx.x * 64 + (k)) * 8 + (ev)] = clock64();    \
   } while (0)
 
-template <bool SPLIT>
+// rows of a tile used by its sequences (last one unpadded)
+__device__ __forceinline__ int att_tile_rows(const AttTile& t) {
+  int o = 0, n = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (t.len[j] > 0) n = o + t.len[j];
+    o += (t.len[j] + 31) & ~31;
+  }
+  return n;
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(ATQ_THREADS, 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap mh,
-                        const __grid_constant__ CUtensorMap ml, const int2* __restrict__ tiles,
-                        const int2* __restrict__ rng, int n_items, int heads, int d, float scale,
+                        const __grid_constant__ CUtensorMap ml, const AttTile* __restrict__ tiles,
+                        int n_items, int heads, int d, float scale,
                         int fmt, uint16_t* __restrict__ ch, uint16_t* __restrict__ cl, int ldc) {
-  using C = AtqCfg<SPLIT>;
+  using C = AtqCfg<MODE>;
+  constexpr bool SPLIT = MODE == 3;     // Q, K, V as hi/lo pairs
+  constexpr bool PSPLIT = MODE >= 2;    // P as hi/lo pair
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
@@ -147,28 +168,43 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
       if (SPLIT) tma_prefetch(&ml);
       for (int k = 0; k < mine; ++k) {
         const int it = item_of(k);
-        const int2 tl = tiles[it / heads];
+        const AttTile tl = tiles[it / heads];
         const int h = it % heads;
         const int cq = h * 64, ck = d + h * 64, cv = 2 * d + h * 64;
+        int rows32 = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) rows32 += (tl.len[j] + 31) & ~31;
         {
           const int s = k % C::QK_ST;
           mbar_wait(&qk_empty[s], ((k / C::QK_ST) & 1) ^ 1);
-          mbar_expect_tx(&qk_full[s], C::QK_BYTES);
+          mbar_expect_tx(&qk_full[s], rows32 * 128 * (SPLIT ? 4 : 2));
           uint8_t* t = sm + s * C::QK_BYTES;
-          tma_load_2d(t, &mh, &qk_full[s], cq, tl.x);
-          tma_load_2d(t + ATQ_TILE, &mh, &qk_full[s], ck, tl.x);
-          if (SPLIT) {
-            tma_load_2d(t + 2 * ATQ_TILE, &ml, &qk_full[s], cq, tl.x);
-            tma_load_2d(t + 3 * ATQ_TILE, &ml, &qk_full[s], ck, tl.x);
+          int o = 0;
+          for (int j = 0; j < 4; ++j) {
+            for (int r0 = 0; r0 < tl.len[j]; r0 += 32, o += 32) {
+              const int tok = tl.t0[j] + r0;
+              tma_load_2d(t + o * 128, &mh, &qk_full[s], cq, tok);
+              tma_load_2d(t + ATQ_TILE + o * 128, &mh, &qk_full[s], ck, tok);
+              if (SPLIT) {
+                tma_load_2d(t + 2 * ATQ_TILE + o * 128, &ml, &qk_full[s], cq, tok);
+                tma_load_2d(t + 3 * ATQ_TILE + o * 128, &ml, &qk_full[s], ck, tok);
+              }
+            }
           }
         }
         {
           const int s = k % C::V_ST;
           mbar_wait(&v_empty[s], ((k / C::V_ST) & 1) ^ 1);
-          mbar_expect_tx(&v_full[s], C::V_BYTES);
+          mbar_expect_tx(&v_full[s], rows32 * 128 * (SPLIT ? 2 : 1));
           uint8_t* t = sm + C::QK_ST * C::QK_BYTES + s * C::V_BYTES;
-          tma_load_2d(t, &mh, &v_full[s], cv, tl.x);
-          if (SPLIT) tma_load_2d(t + ATQ_TILE, &ml, &v_full[s], cv, tl.x);
+          int o = 0;
+          for (int j = 0; j < 4; ++j) {
+            for (int r0 = 0; r0 < tl.len[j]; r0 += 32, o += 32) {
+              const int tok = tl.t0[j] + r0;
+              tma_load_2d(t + o * 128, &mh, &v_full[s], cv, tok);
+              if (SPLIT) tma_load_2d(t + ATQ_TILE + o * 128, &ml, &v_full[s], cv, tok);
+            }
+          }
         }
       }
     }
@@ -180,8 +216,7 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
       // that the group finished reading O(k-2)).
       auto issue_s = [&](int k) {
         const int b = k & 1;
-        const int2 tl = tiles[item_of(k) / heads];
-        const int n16 = (tl.y + 15) & ~15;
+        const int n16 = (att_tile_rows(tiles[item_of(k) / heads]) + 15) & ~15;
         const int s = k % C::QK_ST;
         const uint32_t idesc = idesc_f16kind(128, n16, fmt);
         uint8_t* t = sm + s * C::QK_BYTES;
@@ -203,8 +238,7 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
       };
       auto issue_o = [&](int k) {
         const int b = k & 1;
-        const int2 tl = tiles[item_of(k) / heads];
-        const int n16 = (tl.y + 15) & ~15;
+        const int n16 = (att_tile_rows(tiles[item_of(k) / heads]) + 15) & ~15;
         const int s = k % C::V_ST;
         const uint32_t idesc = idesc_f16kind(128, 64, fmt) | (1u << 16);  // B MN-major
         uint8_t* t = sm + C::QK_ST * C::QK_BYTES + s * C::V_BYTES;
@@ -213,9 +247,9 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
           const uint32_t ph_ = tp + 32 * (kk >> 5) + 8 * ((kk >> 4) & 1);
           const uint64_t vh = umma_desc_sw128(t + kk * 128);
           tc_mma_ts(to, ph_, vh, idesc, kk != 0);
+          if (PSPLIT) tc_mma_ts(to, ph_ + 16, vh, idesc, 1);
           if (SPLIT) {
             const uint64_t vl = umma_desc_sw128(t + ATQ_TILE + kk * 128);
-            tc_mma_ts(to, ph_ + 16, vh, idesc, 1);
             tc_mma_ts(to, ph_, vl, idesc, 1);
           }
         }
@@ -260,14 +294,25 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
     for (int k = g; k < mine; k += 2) {
       const int b = g;
       const int it = item_of(k);
-      const int2 tl = tiles[it / heads];
+      const AttTile tl = tiles[it / heads];
       const int h = it % heads;
-      const int n = tl.y, n16 = (n + 15) & ~15;
-      int ks = 0, ke = 0;
-      if (r < n) {
-        const int2 rr = rng[tl.x + r];
-        ks = rr.x - tl.x;
-        ke = rr.y - tl.x;
+      const int n = att_tile_rows(tl), n16 = (n + 15) & ~15;
+      // this row's sequence: keys [ks, ke) of the tile, token index tok
+      int ks = 0, ke = 0, tok = -1;
+      {
+        int o = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int L = tl.len[j], R = (L + 31) & ~31;
+          if (r >= o && r < o + R) {
+            if (r - o < L) {
+              ks = o;
+              ke = o + L;
+              tok = tl.t0[j] + (r - o);
+            }
+          }
+          o += R;
+        }
       }
       mbar_wait(&s_full[b], (k >> 1) & 1);
       const bool tr = hf == 0 && q == 0 && lane == 0;
@@ -277,7 +322,7 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
       float sum = 1.f;
       if (active) {
         const uint32_t trow = tm + b * 128 + lane_off;
-        int lo = r < n ? ks : 1 << 20, hi = r < n ? ke : 0;
+        int lo = tok >= 0 ? ks : 1 << 20, hi = tok >= 0 ? ke : 0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
@@ -330,7 +375,7 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
                 for (int i = 0; i < 8; ++i) hh[i] = ll[i] = 0u;
               }
               tmem_st_8(trow + c * 32 + half * 8, hh);
-              if (SPLIT) tmem_st_8(trow + c * 32 + 16 + half * 8, ll);
+              if (PSPLIT) tmem_st_8(trow + c * 32 + 16 + half * 8, ll);
             }
           }
         }
@@ -352,9 +397,9 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
         float v[32];
         tmem_ld_32x32(tm + lane_off + 256 + b * 64 + hf * 32, v);
         const float inv = 1.0f / (tmem_ld_1(tmax + 2) + tmem_ld_1(tmax + 3));
-        if (r < n) {
+        if (tok >= 0) {
           // ctx is a convex combination of range-checked V rows: no fp16 overflow possible
-          const size_t ob = (size_t)(tl.x + r) * ldc + h * 64 + hf * 32;
+          const size_t ob = (size_t)tok * ldc + h * 64 + hf * 32;
           uint32_t hh[16], ll[16];
 #pragma unroll
           for (int i = 0; i < 32; i += 2) split2(v[i] * inv, v[i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
@@ -381,65 +426,61 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
   }
 }
 
-// rng[t] = [start, end) of the sequence containing token t (one CTA per sequence).
-__global__ void token_ranges_kernel(const int32_t* __restrict__ cu, int2* __restrict__ rng) {
-  const int a = cu[blockIdx.x], e = cu[blockIdx.x + 1];
-  for (int t = a + threadIdx.x; t < e; t += blockDim.x) rng[t] = make_int2(a, e);
-}
-
 cudaError_t att_set_trace(long long* dev_buf) {
   return cudaMemcpyToSymbol(g_att_trace, &dev_buf, sizeof(dev_buf));
 }
 
-cudaError_t launch_token_ranges(const int32_t* cu, int nseq, int2* rng, cudaStream_t st) {
-  if (nseq <= 0) return cudaSuccess;
-  token_ranges_kernel<<<nseq, 128, 0, st>>>(cu, rng);
-  return cudaGetLastError();
-}
-
-void att_plan_tiles(const int32_t* cu, int nseq, bool tc_ok, std::vector<int2>& tiles,
+void att_plan_tiles(const int32_t* cu, int nseq, bool tc_ok, std::vector<AttTile>& tiles,
                     std::vector<int2>& work) {
   tiles.clear();
   work.clear();
-  int t0 = -1, n = 0;
+  AttTile cur{};
+  int used = 0, nslot = 0;  // 32-row granules used, sequences in `cur`
   for (int s = 0; s < nseq; ++s) {
     const int a = cu[s], L = cu[s + 1] - a;
     if (!tc_ok || L > 128) {
       for (int q = 0; q < L; q += 64) work.push_back(make_int2(s, q));
       continue;
     }
-    if (t0 >= 0 && a == t0 + n && n + L <= 128) {
-      n += L;
-    } else {
-      if (t0 >= 0) tiles.push_back(make_int2(t0, n));
-      t0 = a;
-      n = L;
+    const int R = (L + 31) & ~31;
+    if (nslot == 4 || used + R > 128) {
+      tiles.push_back(cur);
+      cur = AttTile{};
+      used = nslot = 0;
     }
+    cur.t0[nslot] = a;
+    cur.len[nslot] = L;
+    ++nslot;
+    used += R;
   }
-  if (t0 >= 0) tiles.push_back(make_int2(t0, n));
+  if (nslot) tiles.push_back(cur);
 }
 
-cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml, bool split,
-                                const int2* tiles, int n_tiles, const int2* rng, int heads, int d,
+template <int MODE>
+static void att_launch_tc(const CUtensorMap* mh, const CUtensorMap* ml, const AttTile* tiles,
+                          int n_items, int heads, int d, float scale, int fmt,
+                          uint16_t* ch, uint16_t* cl, int ldc, int grid, cudaStream_t st) {
+  constexpr int SM = AtqCfg<MODE>::SMEM;
+  cudaFuncSetAttribute(attention_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
+  attention_tc_kernel<MODE><<<grid, ATQ_THREADS, SM, st>>>(*mh, *ml, tiles, n_items, heads, d,
+                                                           scale, fmt, ch, cl, ldc);
+}
+
+cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml, int mode,
+                                const AttTile* tiles, int n_tiles, int heads, int d,
                                 int fmt, uint16_t* ch, uint16_t* cl, int ldc, int* ovf,
                                 int num_sms, cudaStream_t st) {
+  (void)ovf;  // ctx is a convex combination of range-checked V rows
   if (n_tiles <= 0) return cudaSuccess;
   const float scale = 1.0f / sqrtf((float)d / (float)heads);
   const int n_items = n_tiles * heads;
   const int grid = n_items < num_sms ? n_items : num_sms;
-  if (split) {
-    constexpr int SM = AtqCfg<true>::SMEM;
-    cudaFuncSetAttribute(attention_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SM);
-    attention_tc_kernel<true><<<grid, ATQ_THREADS, SM, st>>>(
-        *mh, *ml, tiles, rng, n_items, heads, d, scale, fmt, ch, cl, ldc);
-  } else {
-    constexpr int SM = AtqCfg<false>::SMEM;
-    cudaFuncSetAttribute(attention_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SM);
-    attention_tc_kernel<false><<<grid, ATQ_THREADS, SM, st>>>(
-        *mh, *mh, tiles, rng, n_items, heads, d, scale, fmt, ch, cl, ldc);
-  }
+  if (mode == 3)
+    att_launch_tc<3>(mh, ml, tiles, n_items, heads, d, scale, fmt, ch, cl, ldc, grid, st);
+  else if (mode == 2)
+    att_launch_tc<2>(mh, mh, tiles, n_items, heads, d, scale, fmt, ch, cl, ldc, grid, st);
+  else
+    att_launch_tc<1>(mh, mh, tiles, n_items, heads, d, scale, fmt, ch, cl, ldc, grid, st);
   return cudaGetLastError();
 }
 

@@ -46,7 +46,12 @@ struct GemmArgs {
   int ldh;
   int fmt;                   // FMT_F16 / FMT_BF16: operand format of A, B and out_hi/lo
   int* ovf;                  // set to 1 when an fp16 output overflows
+  int r16;                   // reference binary16 mode (`encoder.py:120-126`): round the
+                             // product to fp16, add the fp16 bias in fp16, round residual
+                             // sums to fp16 (bias must hold fp16-representable values)
 };
+
+__device__ __forceinline__ float round16(float v) { return __half2float(__float2half_rn(v)); }
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
@@ -107,11 +112,20 @@ __device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, in
       const int r = it * 4 + rs;
       if (r < rows) {
         const float* src = buf + r * 33 + 4 * cg;
-        float x[4] = {src[0] + b.x, src[1] + b.y, src[2] + b.z, src[3] + b.w};
+        float x[4];
+        if (args.r16) {
+          x[0] = round16(round16(src[0]) + b.x); x[1] = round16(round16(src[1]) + b.y);
+          x[2] = round16(round16(src[2]) + b.z); x[3] = round16(round16(src[3]) + b.w);
+        } else {
+          x[0] = src[0] + b.x; x[1] = src[1] + b.y; x[2] = src[2] + b.z; x[3] = src[3] + b.w;
+        }
         const size_t o = (size_t)(row0 + r);
         if (EPI == EPI_F32 || EPI == EPI_F32_RES) {
           if (EPI == EPI_F32_RES) {
             x[0] += res[it].x; x[1] += res[it].y; x[2] += res[it].z; x[3] += res[it].w;
+            if (args.r16) {
+              x[0] = round16(x[0]); x[1] = round16(x[1]); x[2] = round16(x[2]); x[3] = round16(x[3]);
+            }
           }
           *reinterpret_cast<float4*>(args.out_f32 + o * args.ldo + col) =
               make_float4(x[0], x[1], x[2], x[3]);

@@ -16,7 +16,7 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __r
                              int V, int d, const float* __restrict__ tok,
                              const float* __restrict__ pe, float* __restrict__ x32, int ld,
                              uint16_t* __restrict__ xh, uint16_t* __restrict__ xl, int fmt,
-                             int* flag) {
+                             int r16, int* flag) {
   const int start = cu[blockIdx.x], end = cu[blockIdx.x + 1];
   const int lane = threadIdx.x & 31;
   for (int t = start + (threadIdx.x >> 5); t < end; t += blockDim.x >> 5) {
@@ -29,7 +29,8 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __r
     const float* b = pe + (size_t)(t - start) * d;
     const size_t o = (size_t)t * ld;
     for (int c = lane; c < d; c += 32) {
-      const float v = a[c] + b[c];
+      float v = a[c] + b[c];
+      if (r16) v = __half2float(__float2half_rn(v));  // binary16 add (reference fp16 mode)
       x32[o + c] = v;
       if (xh) store_split(xh, xl, o + c, v, fmt, flag);
     }
@@ -45,7 +46,7 @@ __global__ void __launch_bounds__(256)
     layernorm_kernel(const float* __restrict__ y, int T, int d, int ld,
                      const float* __restrict__ g, const float* __restrict__ bta,
                      float* __restrict__ out32, uint16_t* __restrict__ oh,
-                     uint16_t* __restrict__ ol, int fmt, int* ovf) {
+                     uint16_t* __restrict__ ol, int fmt, int r16, int* ovf) {
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -77,8 +78,12 @@ __global__ void __launch_bounds__(256)
     if (c < n4) {
       const float4 gg = reinterpret_cast<const float4*>(g)[c];
       const float4 bb = reinterpret_cast<const float4*>(bta)[c];
-      const float r[4] = {(v[i].x - mean) * rstd * gg.x + bb.x, (v[i].y - mean) * rstd * gg.y + bb.y,
-                          (v[i].z - mean) * rstd * gg.z + bb.z, (v[i].w - mean) * rstd * gg.w + bb.w};
+      float r[4] = {(v[i].x - mean) * rstd * gg.x + bb.x, (v[i].y - mean) * rstd * gg.y + bb.y,
+                    (v[i].z - mean) * rstd * gg.z + bb.z, (v[i].w - mean) * rstd * gg.w + bb.w};
+      if (r16) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[j] = __half2float(__float2half_rn(r[j]));
+      }
       if (out32) reinterpret_cast<float4*>(out32 + o)[c] = make_float4(r[0], r[1], r[2], r[3]);
       if (oh) {
         uint16_t h[4], l[4];
@@ -99,7 +104,7 @@ __global__ void __launch_bounds__(256)
 __global__ void layernorm_scalar_kernel(const float* __restrict__ y, int T, int d, int ld,
                                         const float* __restrict__ g, const float* __restrict__ bta,
                                         float* __restrict__ out32, uint16_t* __restrict__ oh,
-                                        uint16_t* __restrict__ ol, int fmt, int* ovf) {
+                                        uint16_t* __restrict__ ol, int fmt, int r16, int* ovf) {
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -112,7 +117,8 @@ __global__ void layernorm_scalar_kernel(const float* __restrict__ y, int T, int 
   const float rstd = 1.0f / sqrtf(warp_sum(q) / (float)d + 1e-5f);
   const size_t o = (size_t)t * ld;
   for (int c = lane; c < d; c += 32) {
-    const float r = (row[c] - mean) * rstd * g[c] + bta[c];
+    float r = (row[c] - mean) * rstd * g[c] + bta[c];
+    if (r16) r = __half2float(__float2half_rn(r));
     if (out32) out32[o + c] = r;
     if (oh) store_split(oh, ol, o + c, r, fmt, ovf);
   }
@@ -359,14 +365,14 @@ __global__ void gather_col0_kernel(const float* __restrict__ out, int ld, int n,
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_embed(const int32_t* ids, const int32_t* cu, int nseq, int V, int d,
                          const float* tok, const float* pe, float* x32, int ld, uint16_t* xh,
-                         uint16_t* xl, int fmt, int* flag, cudaStream_t st) {
+                         uint16_t* xl, int fmt, int r16, int* flag, cudaStream_t st) {
   if (nseq <= 0) return cudaSuccess;
-  embed_kernel<<<nseq, 256, 0, st>>>(ids, cu, V, d, tok, pe, x32, ld, xh, xl, fmt, flag);
+  embed_kernel<<<nseq, 256, 0, st>>>(ids, cu, V, d, tok, pe, x32, ld, xh, xl, fmt, r16, flag);
   return cudaGetLastError();
 }
 
 cudaError_t launch_layernorm(const float* y, int T, int d, int ld, const float* g, const float* b,
-                             float* out32, uint16_t* oh, uint16_t* ol, int fmt, int* ovf,
+                             float* out32, uint16_t* oh, uint16_t* ol, int fmt, int r16, int* ovf,
                              cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
   dim3 grid((T + 7) / 8), block(256);
@@ -376,14 +382,14 @@ cudaError_t launch_layernorm(const float* y, int T, int d, int ld, const float* 
   if (vec) {
 #define LN_CASE(V)                                                                   \
     if (v4 <= V) {                                                                   \
-      layernorm_kernel<V><<<grid, block, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol, fmt, ovf); \
+      layernorm_kernel<V><<<grid, block, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol, fmt, r16, ovf); \
       return cudaGetLastError();                                                     \
     }
     LN_CASE(1) LN_CASE(2) LN_CASE(4) LN_CASE(8) LN_CASE(9) LN_CASE(10) LN_CASE(12) LN_CASE(16)
     LN_CASE(20) LN_CASE(24) LN_CASE(32)
 #undef LN_CASE
   }
-  layernorm_scalar_kernel<<<grid, block, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol, fmt, ovf);
+  layernorm_scalar_kernel<<<grid, block, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol, fmt, r16, ovf);
   return cudaGetLastError();
 }
 

@@ -11,9 +11,9 @@ namespace mfg {
 
 cudaError_t launch_embed(const int32_t* ids, const int32_t* cu, int nseq, int V, int d,
                          const float* tok, const float* pe, float* x32, int ld, uint16_t* xh,
-                         uint16_t* xl, int fmt, int* flag, cudaStream_t st);
+                         uint16_t* xl, int fmt, int r16, int* flag, cudaStream_t st);
 cudaError_t launch_layernorm(const float* y, int T, int d, int ld, const float* g, const float* b,
-                             float* out32, uint16_t* oh, uint16_t* ol, int fmt, int* ovf,
+                             float* out32, uint16_t* oh, uint16_t* ol, int fmt, int r16, int* ovf,
                              cudaStream_t st);
 // SIMT fp32 attention over (sequence, 64-query block) work items; Q|K|V read as
 // hi(+lo) 16-bit pieces [T][ldq].
@@ -21,19 +21,23 @@ cudaError_t launch_attention(const uint16_t* qh, const uint16_t* ql, int ldq, in
                              const int32_t* cu,
                              const int2* work, int n_work, uint16_t* ch, uint16_t* cl,
                              int ldc, int fmt, int* ovf, cudaStream_t st);
-// Persistent tcgen05 attention over (tile, head) items; tiles pack whole
-// sequences of <= 128 tokens into <= 128 consecutive rows (att_plan_tiles),
-// d_head == 64. Maps: Q|K|V hi/lo [T][ldq] with box {64 cols, 128 rows};
-// rng[t] = [start, end) of token t's sequence (launch_token_ranges).
-cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml, bool split,
-                                const int2* tiles, int n_tiles, const int2* rng, int heads, int d,
-                                int fmt, uint16_t* ch, uint16_t* cl, int ldc, int* ovf,
-                                int num_sms, cudaStream_t st);
+// Persistent tcgen05 attention over (tile, head) items, d_head == 64. A tile
+// holds up to 4 whole sequences of <= 128 tokens at 32-aligned tile rows
+// (att_plan_tiles). Maps: Q|K|V hi/lo [T][ldq] with box {64 cols, 32 rows}.
+// mode: 3 = Q/K/V and P as hi/lo pairs (3 MMAs per product), 2 = single Q/K/V,
+// P as hi/lo (reference fp16 mode), 1 = everything single (bf16 mode).
+struct AttTile {
+  int t0[4];   // first token of each sequence (packed stream index)
+  int len[4];  // its length (0 = unused slot)
+};
+cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml, int mode,
+                                const AttTile* tiles, int n_tiles, int heads, int d, int fmt,
+                                uint16_t* ch, uint16_t* cl, int ldc, int* ovf, int num_sms,
+                                cudaStream_t st);
 cudaError_t att_set_trace(long long* dev_buf);  // diagnostics: [4][64][8] clock64 or null
-cudaError_t launch_token_ranges(const int32_t* cu, int nseq, int2* rng, cudaStream_t st);
-// Host: sequences of <= 128 tokens (when tc_ok) -> packed tiles {t0, rows};
-// the rest -> SIMT work items {seq, q0} (64-query blocks).
-void att_plan_tiles(const int32_t* cu, int nseq, bool tc_ok, std::vector<int2>& tiles,
+// Host: sequences of <= 128 tokens (when tc_ok) -> tiles; the rest -> SIMT
+// work items {seq, q0} (64-query blocks).
+void att_plan_tiles(const int32_t* cu, int nseq, bool tc_ok, std::vector<AttTile>& tiles,
                     std::vector<int2>& work);
 cudaError_t launch_features(const float* x, int ld, int d, int kind, const int32_t* cu, int n,
                             uint16_t* fh, uint16_t* fl, int ldf, int fmt, int* ovf,

@@ -75,6 +75,7 @@ enum Cls { C_QKV = 0, C_O, C_FFN1, C_FFN2, C_ATT, C_LN, C_EMB, C_HEAD };
 struct mfg_ctx {
   int device = 0, precision = MFG_PREC_FP32, num_sms = 148;
   bool split = true, pre_norm = false, profile = false;
+  bool r16 = false;        // reference binary16 mode: every tensor and activation is fp16
   int fmt = FMT_F16;       // 16-bit operand format of every GEMM operand
   int* d_ovf = nullptr;    // fp16 range overflow flag (set by any producer)
   int* h_ovf = nullptr;
@@ -95,9 +96,10 @@ struct mfg_ctx {
   float *x32 = nullptr, *y32 = nullptr;
   Act xa, ca, ha, fa, qa;          // qa: Q|K|V pieces [T][qkv_ld]
   bool att_tc = false;              // tcgen05 attention usable (d_head == 64)
-  int2 *d_tiles = nullptr, *h_tiles = nullptr;  // packed attention tiles {t0, rows}
-  int2* d_rng = nullptr;            // per token: [start, end) of its sequence
-  std::vector<int2> v_tiles, v_work;
+  AttTile *d_tiles = nullptr, *h_tiles = nullptr;  // attention tiles (att_plan_tiles)
+  CUtensorMap qm32h{}, qm32l{};     // Q|K|V maps with 32-row boxes (attention tiles)
+  std::vector<AttTile> v_tiles;
+  std::vector<int2> v_work;
   std::vector<Act> ga;  // head hidden-stage outputs
   float* hout = nullptr;
   float* dscores = nullptr;
@@ -205,7 +207,7 @@ struct mfg_ctx {
     w.bias = dalloc<float>(w.Npad);
     int off = 0;
     for (auto* b : biases) {
-      const float* src = host_f32(*b, host_tmp);
+      const float* src = host_vec(*b, host_tmp);
       CK(cudaMemcpy(w.bias + off, src, b->numel() * 4, cudaMemcpyHostToDevice));
       off += (int)b->numel();
     }
@@ -237,9 +239,18 @@ struct mfg_ctx {
     return tmp.data();
   }
 
+  // fp32 view of a vector/table; in binary16 mode rounded like `tensor.astype(float16)`
+  // (`encoder.py:102-118`) — GEMM weights get the same rounding from transpose_split.
+  const float* host_vec(const TensorView& t, std::vector<float>& tmp) const {
+    const float* src = host_f32(t, tmp);
+    if (!r16) return src;
+    if (src != tmp.data()) tmp.assign(src, src + t.numel());
+    for (auto& v : tmp) v = __half2float(__float2half_rn(v));
+    return tmp.data();
+  }
   float* upload_vec(const TensorView& t, size_t pad_to = 0) {
     std::vector<float> tmp;
-    const float* src = host_f32(t, tmp);
+    const float* src = host_vec(t, tmp);
     float* p = dalloc<float>(std::max<size_t>(pad_to, (size_t)t.numel()));
     CK(cudaMemcpy(p, src, t.numel() * 4, cudaMemcpyHostToDevice));
     return p;
@@ -327,6 +338,13 @@ struct mfg_ctx {
     x32 = dalloc<float>((size_t)cap_tokens * dp);
     y32 = dalloc<float>((size_t)cap_tokens * dp);
     make_act(qa, cap_tokens, qkv_ld);
+    {
+      char err[256];
+      if (!make_tmap_u16(&qm32h, qa.hi, qa.rows, qa.ld, qa.ld, 32, err, sizeof err))
+        throw Fail{MFG_ERR_RUNTIME, err};
+      if (split && !make_tmap_u16(&qm32l, qa.lo, qa.rows, qa.ld, qa.ld, 32, err, sizeof err))
+        throw Fail{MFG_ERR_RUNTIME, err};
+    }
     att_tc = (d / H == 64) && (d % 64 == 0);
     make_act(xa, cap_tokens, dp);
     make_act(ca, cap_tokens, dp);
@@ -338,9 +356,8 @@ struct mfg_ctx {
     dscores = dalloc<float>(cap_records);
     d_ids = dalloc<int32_t>(cap_tokens);
     d_cu = dalloc<int32_t>((size_t)cap_records * n_roles + 1);
-    d_tiles = dalloc<int2>((size_t)cap_records * n_roles);
-    CK(cudaMallocHost(&h_tiles, (size_t)cap_records * n_roles * sizeof(int2)));
-    d_rng = dalloc<int2>(cap_tokens);
+    d_tiles = dalloc<AttTile>((size_t)cap_records * n_roles);
+    CK(cudaMallocHost(&h_tiles, (size_t)cap_records * n_roles * sizeof(AttTile)));
     work_cap = cap_tokens / 1 + (int64_t)cap_records * n_roles;
     d_work = dalloc<int2>(work_cap);
     CK(cudaMallocHost(&h_ids, cap_tokens * 4));
@@ -366,6 +383,7 @@ struct mfg_ctx {
     g.ldo = ldo;
     g.fmt = fmt;
     g.ovf = d_ovf;
+    g.r16 = r16;
     if (outa) {
       g.out_hi = outa->hi;
       g.out_lo = outa->lo;
@@ -383,7 +401,7 @@ struct mfg_ctx {
   void layernorm(const float* y, int T, const float* g, const float* b, float* out32, Act* a) {
     int e = ev_begin();
     CK(launch_layernorm(y, T, d, dp, g, b, out32, a ? a->hi : nullptr, a ? a->lo : nullptr, fmt,
-                        d_ovf, st));
+                        r16, d_ovf, st));
     ev_end(e, C_LN, 0, (double)T * d * (4 + (out32 ? 4 : 0) + (a ? (split ? 4 : 2) : 0)));
   }
 
@@ -393,10 +411,8 @@ struct mfg_ctx {
   void forward_chunk(int m, int64_t T, int64_t n_work, int n_tiles, double sum_l2) {
     const int nseq = m * n_roles;
     CK(cudaMemcpyAsync(d_cu, h_cu, (nseq + 1) * 4, cudaMemcpyHostToDevice, st));
-    if (n_tiles > 0) {
-      CK(cudaMemcpyAsync(d_tiles, h_tiles, n_tiles * sizeof(int2), cudaMemcpyHostToDevice, st));
-      CK(launch_token_ranges(d_cu, nseq, d_rng, st));
-    }
+    if (n_tiles > 0)
+      CK(cudaMemcpyAsync(d_tiles, h_tiles, n_tiles * sizeof(AttTile), cudaMemcpyHostToDevice, st));
     if (n_work > 0)
       CK(cudaMemcpyAsync(d_work, h_work, n_work * sizeof(int2), cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(d_ovf, 0, sizeof(int), st));
@@ -404,7 +420,7 @@ struct mfg_ctx {
     {
       int e = ev_begin();
       CK(launch_embed(d_ids, d_cu, nseq, (int)man.vocab_size, d, tok, pos, x32, dp,
-                      pre_norm ? nullptr : xa.hi, pre_norm ? nullptr : xa.lo, fmt, d_ovf, st));
+                      pre_norm ? nullptr : xa.hi, pre_norm ? nullptr : xa.lo, fmt, r16, d_ovf, st));
       ev_end(e, C_EMB, 0, (double)T * d * (8 + 4 + (pre_norm ? 0 : (split ? 4 : 2))));
     }
     for (auto& L : layers) {
@@ -414,8 +430,8 @@ struct mfg_ctx {
         const double bytes = (double)T * d * 4 * (split ? 4 : 2);
         int e = ev_begin();
         if (n_tiles > 0)
-          CK(launch_attention_tc(&qa.mh, split ? &qa.ml : &qa.mh, split, d_tiles, n_tiles, d_rng,
-                                 H, d, fmt, ca.hi, ca.lo, ca.ld, d_ovf, num_sms, st));
+          CK(launch_attention_tc(&qm32h, split ? &qm32l : &qm32h, split ? 3 : r16 ? 2 : 1, d_tiles,
+                                 n_tiles, H, d, fmt, ca.hi, ca.lo, ca.ld, d_ovf, num_sms, st));
         if (n_work > 0)
           CK(launch_attention(qa.hi, qa.lo, qa.ld, d, H, d_cu, d_work, (int)n_work, ca.hi, ca.lo,
                               ca.ld, fmt, d_ovf, st));
@@ -587,12 +603,13 @@ extern "C" int mfg_create(const mfg_config* cfg, mfg_ctx** out) {
   *out = nullptr;
   mfg_ctx* c = new mfg_ctx();
   try {
-    if (cfg->precision < MFG_PREC_FP32 || cfg->precision > MFG_PREC_BF16X3)
+    if (cfg->precision < MFG_PREC_FP32 || cfg->precision > MFG_PREC_FP16)
       throw Fail{MFG_ERR_USAGE, "unknown precision " + std::to_string(cfg->precision)};
     c->device = cfg->device;
     c->precision = cfg->precision;
-    c->split = cfg->precision != MFG_PREC_BF16;
-    c->fmt = cfg->precision == MFG_PREC_FP32 ? FMT_F16 : FMT_BF16;
+    c->split = cfg->precision == MFG_PREC_FP32 || cfg->precision == MFG_PREC_BF16X3;
+    c->r16 = cfg->precision == MFG_PREC_FP16;
+    c->fmt = (cfg->precision == MFG_PREC_FP32 || c->r16) ? FMT_F16 : FMT_BF16;
     c->profile = cfg->profile != 0;
     CK(cudaSetDevice(c->device));
     int major = 0, minor = 0;
@@ -766,8 +783,9 @@ extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, i
                          const float* A, const float* W, const float* bias,
                          const float* residual, float* out) {
   return guarded([&] {
-    const bool split = precision != MFG_PREC_BF16;
-    const int fmt = precision == MFG_PREC_FP32 ? FMT_F16 : FMT_BF16;
+    const bool split = precision == MFG_PREC_FP32 || precision == MFG_PREC_BF16X3;
+    const bool r16 = precision == MFG_PREC_FP16;
+    const int fmt = (precision == MFG_PREC_FP32 || r16) ? FMT_F16 : FMT_BF16;
     int dev = 0, sms = 148;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -789,7 +807,12 @@ extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, i
     CK(cudaGetLastError());
     CK(launch_transpose_split(dW, K, N, wh, wl, Kp, 0, fmt, nullptr, 0));
     float* db = s.alloc<float>(Np);
-    if (bias) CK(cudaMemcpy(db, bias, N * 4, cudaMemcpyHostToDevice));
+    if (bias) {
+      std::vector<float> b(bias, bias + N);
+      if (r16)
+        for (auto& v : b) v = __half2float(__float2half_rn(v));
+      CK(cudaMemcpy(db, b.data(), N * 4, cudaMemcpyHostToDevice));
+    }
     float* dr = s.alloc<float>((size_t)M * Np);
     if (residual)
       CK(cudaMemcpy2D(dr, Np * 4, residual, N * 4, N * 4, M, cudaMemcpyHostToDevice));
@@ -817,6 +840,7 @@ extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, i
     g.ldh = Np;
     g.fmt = fmt;
     g.ovf = nullptr;
+    g.r16 = r16;
     CK(launch_gemm(&mah, split ? &mal : &mah, &mwh, split ? &mwl : &mwh, bn, split ? 2 : 1, epi,
                    g, sms, 0));
     CK(cudaDeviceSynchronize());
@@ -834,8 +858,9 @@ extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, i
 extern "C" int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* cu, int32_t d,
                               int32_t n_heads, const float* qkv, float* ctx_out, int32_t use_tc) {
   return guarded([&] {
-    const bool split = precision != MFG_PREC_BF16;
-    const int fmt = precision == MFG_PREC_FP32 ? FMT_F16 : FMT_BF16;
+    const bool split = precision == MFG_PREC_FP32 || precision == MFG_PREC_BF16X3;
+    const bool r16 = precision == MFG_PREC_FP16;
+    const int fmt = (precision == MFG_PREC_FP32 || r16) ? FMT_F16 : FMT_BF16;
     Scratch s;
     char err[256];
     const int T = cu[n_seq];
@@ -851,28 +876,27 @@ extern "C" int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* c
     int32_t* dcu = s.alloc<int32_t>(n_seq + 1);
     CK(cudaMemcpy(dcu, cu, (n_seq + 1) * 4, cudaMemcpyHostToDevice));
     const bool tc_ok = use_tc && (d / n_heads == 64) && (d % 64 == 0);
-    std::vector<int2> work, tiles;
+    std::vector<int2> work;
+    std::vector<AttTile> tiles;
     att_plan_tiles(cu, n_seq, tc_ok, tiles, work);
     int2* dw = s.alloc<int2>(work.size());
     if (!work.empty())
       CK(cudaMemcpy(dw, work.data(), work.size() * sizeof(int2), cudaMemcpyHostToDevice));
-    int2* dt = s.alloc<int2>(tiles.size());
+    AttTile* dt = s.alloc<AttTile>(tiles.size());
     if (!tiles.empty())
-      CK(cudaMemcpy(dt, tiles.data(), tiles.size() * sizeof(int2), cudaMemcpyHostToDevice));
-    int2* drng = s.alloc<int2>(T);
-    CK(launch_token_ranges(dcu, n_seq, drng, 0));
+      CK(cudaMemcpy(dt, tiles.data(), tiles.size() * sizeof(AttTile), cudaMemcpyHostToDevice));
     auto* ch = s.alloc<uint16_t>((size_t)T * ldc);
     auto* cl = split ? s.alloc<uint16_t>((size_t)T * ldc) : nullptr;
     if (!tiles.empty()) {
       CUtensorMap mh, ml;
-      if (!make_tmap_u16(&mh, qh, Tp, ldq, ldq, 128, err, sizeof err))
+      if (!make_tmap_u16(&mh, qh, Tp, ldq, ldq, 32, err, sizeof err))
         throw Fail{MFG_ERR_RUNTIME, err};
-      if (split && !make_tmap_u16(&ml, ql, Tp, ldq, ldq, 128, err, sizeof err))
+      if (split && !make_tmap_u16(&ml, ql, Tp, ldq, ldq, 32, err, sizeof err))
         throw Fail{MFG_ERR_RUNTIME, err};
       int sms = 148, dev = 0;
       CK(cudaGetDevice(&dev));
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      CK(launch_attention_tc(&mh, split ? &ml : &mh, split, dt, (int)tiles.size(), drng,
+      CK(launch_attention_tc(&mh, split ? &ml : &mh, split ? 3 : r16 ? 2 : 1, dt, (int)tiles.size(),
                              n_heads, d, fmt, ch, cl, ldc, nullptr, sms, 0));
     }
     if (!work.empty())
@@ -915,7 +939,7 @@ extern "C" int mfgt_layernorm(int32_t T, int32_t d, const float* y, const float*
     CK(cudaMemcpy(dy, y, (size_t)T * d * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dg, g, d * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(db, b, d * 4, cudaMemcpyHostToDevice));
-    CK(launch_layernorm(dy, T, d, d, dg, db, dout, nullptr, nullptr, FMT_BF16, nullptr, 0));
+    CK(launch_layernorm(dy, T, d, d, dg, db, dout, nullptr, nullptr, FMT_BF16, 0, nullptr, 0));
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out, dout, (size_t)T * d * 4, cudaMemcpyDeviceToHost));
   });

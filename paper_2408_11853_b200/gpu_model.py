@@ -12,6 +12,10 @@ Precisions (`EvaluatorConfig.precision`):
             TMEM accumulator (|Δ| ≤ 1e-3 per segment against the fp32 reference)
   "bf16x3"  the same with bf16 pieces (~16 bits, full fp32 range)
   "bf16"    one bf16 MMA per k-step — reported separately with its error stats
+  "fp16"    the reference's own fp16 mode (`encoder.py:105, 120-130`): binary16
+            weights and activations, one fp16 MMA per k-step (fp16 products are
+            exact in the fp32 accumulator), binary16 rounding at every point the
+            reference rounds; selected by `fp16=True` / ComputeMode.FP16
 """
 
 from __future__ import annotations
@@ -27,7 +31,7 @@ from . import native
 from .errors import ContainerError, DeviceError
 from .kinds import N_SEQUENCES, Kind
 
-PRECISIONS = {"fp32": 0, "bf16": 1, "bf16x3": 2}
+PRECISIONS = {"fp32": 0, "bf16": 1, "bf16x3": 2, "fp16": 3}
 
 
 class ComputeMode(enum.Enum):
@@ -46,8 +50,8 @@ class ComputeMode(enum.Enum):
 
 def default_precision(compute_mode) -> str:
     """fp32 keeps the parity path; the reference's fp16 flag (binary16
-    storage) selects the reduced-precision bf16 device path."""
-    return "fp32" if ComputeMode.parse(compute_mode) is ComputeMode.FP32 else "bf16"
+    storage) selects the device path with the same binary16 semantics."""
+    return "fp32" if ComputeMode.parse(compute_mode) is ComputeMode.FP32 else "fp16"
 
 
 def _device_ordinal(device) -> int:
@@ -69,7 +73,8 @@ class GpuScoringModel:
         self.mode = ComputeMode.parse(compute_mode)
         self.precision = precision or default_precision(self.mode)
         if self.precision not in PRECISIONS:
-            raise ValueError(f"unknown precision {self.precision!r} (known: fp32, bf16x3, bf16)")
+            raise ValueError(f"unknown precision {self.precision!r} "
+                             f"(known: {', '.join(PRECISIONS)})")
         self._lib = native.gpu()
         cfg = native.MfgConfig(os.fsencode(str(path)), _device_ordinal(device),
                                PRECISIONS[self.precision], int(max_tokens), int(max_records),

@@ -132,3 +132,38 @@ def test_layernorm_parity(lib, T, d):
     var = ((y64 - mu) ** 2).mean(1, keepdims=True)
     want = (y64 - mu) / np.sqrt(var + 1e-5) * g + b
     assert np.abs(out - want).max() <= 2e-5 * (1 + np.abs(want).max())
+
+
+@pytest.mark.parametrize("M,N,K", [(37, 48, 16), (200, 256, 128), (300, 1024, 1024), (129, 1152, 192)])
+@pytest.mark.parametrize("epi", [0, 1, 2])
+def test_gemm_fp16_reference_mode(lib, M, N, K, epi):
+    """Precision 3 (the reference's fp16 mode): binary16 operands, one MMA per
+    k-step, fp16 rounding of the product, fp16 bias add, fp16 residual sum
+    (`encoder.py:120-126`). fp16 products are exact in fp32, so the device agrees
+    with the reference arithmetic except for rare 1-ulp flips from the fp32
+    summation order."""
+    rng = np.random.default_rng(M + N + K + 10 * epi)
+    h = lambda x: np.asarray(x, np.float32).astype(np.float16)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    W = (rng.standard_normal((K, N)) / math.sqrt(K)).astype(np.float32)
+    b = (0.1 * rng.standard_normal(N)).astype(np.float32)
+    r = h(rng.standard_normal((M, N))).astype(np.float32)
+    got = _gemm(lib, 3, epi, A, W, b, r)
+    prod = h(h(A).astype(np.float64) @ h(W).astype(np.float64))
+    y = h(prod + h(b))                       # numpy float16 + float16 -> float16
+    if epi == 1:
+        y = h(y.astype(np.float32) + r)
+    if epi == 2:
+        c = math.sqrt(2 / math.pi)
+        y32 = y.astype(np.float32)
+        y = h(0.5 * y32 * (1 + np.tanh(c * (y32 + 0.044715 * y32 ** 3))))
+    want = y.astype(np.float64)
+    # a 1-ulp flip of the rounded product propagates through the fp16 bias /
+    # residual adds: bound by the ulp of the largest operand along the chain
+    scale = np.abs(prod.astype(np.float64)) + np.abs(h(b).astype(np.float64)) + np.abs(want)
+    if epi == 1:
+        scale = scale + np.abs(r)
+    ulp = np.spacing(scale.astype(np.float16)).astype(np.float64)
+    d = np.abs(got - want)
+    assert np.all(d <= 3 * ulp + 1e-7), float((d / ulp).max())
+    assert np.mean(d == 0) > 0.97

@@ -206,3 +206,38 @@ def test_fp16_flag_stays_within_reference_bound(golden, tiny_factory):
         r16 = ev.evaluate_lines(lines)
     d = np.abs(np.array(r32.segment_scores) - np.array(r16.segment_scores))
     assert d.max() <= 5e-2 and abs(r32.system_score - r16.system_score) <= 1e-2
+
+
+@pytest.mark.parametrize("key", ["comet-qe/post", "comet-qe/pre", "comet/post", "comet/pre",
+                                 "bleurt/post", "bleurt/pre"])
+def test_fp16_mode_matches_reference_fp16(golden, tiny_factory, key):
+    """`fp16=True` runs the reference's binary16 semantics on the device (fp16
+    MMAs, binary16 rounding at every reference rounding point): scores agree with
+    the reference's own fp16 path far inside its fp32 bound (5e-2)."""
+    g = golden["tiny"][key]
+    kind, style = key.split("/")
+    fix = tiny_factory(kind, style, g["seed"])
+    with make_ev(fix, compute_mode="fp16") as ev:
+        assert ev.model.precision == "fp16"
+        got = ev.evaluate_lines(g["lines"])
+    d = np.abs(np.array(got.segment_scores) - np.array(g["fp16"]))
+    assert d.max() <= 2e-3, d.max()
+    assert abs(got.system_score - g["fp16_system"]) <= 1e-3
+
+
+def test_fp16_mode_midsize_vs_oracle_fp16(golden, fixture_dir):
+    """XLM-R widths (d 1024, 16 heads, ffn 4096, 2 layers): device fp16 mode vs
+    the oracle's fp16 mode (pinned to the reference in test_oracle.py)."""
+    g = golden["midsize"]
+    man = g["manifest"]
+    w = dict(fx.synthetic_weights(man))
+    path = write_model(fixture_dir / "mid16.mfrg", man, w)
+    vpath = fx.write_vocab(fixture_dir / "mid16_vocab.txt", fx.synthetic_vocab_lines(man["vocab_size"]))
+    lines = g["lines"][:24]
+    want, _ = oe.score_lines(OracleModel(man, w, mode="fp16"),
+                             otk.OracleVocab(fx.synthetic_vocab_lines(man["vocab_size"])), lines)
+    with mf.Evaluator(mf.EvaluatorConfig(model=path, vocab=vpath, quiet=True,
+                                         compute_mode="fp16")) as ev:
+        got = ev.evaluate_lines(lines).segment_scores
+    d = np.abs(np.array(got) - np.array(want))
+    assert d.max() <= 2e-3, d.max()
