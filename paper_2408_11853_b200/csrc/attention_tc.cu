@@ -34,8 +34,8 @@
 // Inside a group two warps share each TMEM lane quarter (= 32 tile rows): warp
 // half hf takes the key chunks c with c % 2 == hf and the O columns 32hf..+31;
 // the pair exchanges row max / row sum through TMEM (named barrier).
-// TMEM columns: S/P of region b at 128b..128b+127; O of region b at 256+64b;
-// partial max / sum of region b, half hf at 384+4b+hf / 384+4b+2+hf.
+// TMEM columns: S/P of region b at 128b..128b+127; O of region b at 256+128b
+// (MODE 3: Ph·Vh + Pl·Vh in the first 64 columns, Ph·Vl in the next 64).
 // Measured (tools/mma_probe.cu): a 128xNx16 MMA costs >= ~72 cycles (SS) /
 // ~107 cycles (A from TMEM) for N <= 128, so per item the tensor pipe needs
 // ~1.1k cycles for S and ~2.5k for O.
@@ -58,8 +58,9 @@ struct AtqCfg {
   static constexpr int QK_BYTES = (SPLIT ? 4 : 2) * ATQ_TILE;  // Qh Kh (Ql Kl)
   static constexpr int V_BYTES = (SPLIT ? 2 : 1) * ATQ_TILE;   // Vh (Vl)
   static constexpr int QK_ST = SPLIT ? 2 : 3;
-  static constexpr int V_ST = SPLIT ? 3 : 6;
-  static constexpr int BAR_OFF = QK_ST * QK_BYTES + V_ST * V_BYTES;
+  static constexpr int V_ST = SPLIT ? 2 : 5;
+  static constexpr int RED_OFF = QK_ST * QK_BYTES + V_ST * V_BYTES;  // [group][max|sum][half][row]
+  static constexpr int BAR_OFF = RED_OFF + 2 * 2 * 2 * 128 * 4;
   static constexpr int SMEM = 1024 + BAR_OFF + 256;
   static_assert(SMEM <= 232448, "attention smem");
 };
@@ -69,6 +70,19 @@ __device__ __forceinline__ void tmem_st_8(uint32_t taddr, const uint32_t (&r)[8]
       "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
       : "memory");
+}
+__device__ __forceinline__ void tmem_ld_32x16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void tmem_st_1(uint32_t taddr, uint32_t v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
@@ -144,7 +158,7 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
     }
     for (int s = 0; s < C::V_ST; ++s) {
       mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 1);
+      mbar_init(&v_empty[s], 8);  // released by the 8 warps of the item's group
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
@@ -240,21 +254,24 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
         const int b = k & 1;
         const int n16 = (att_tile_rows(tiles[item_of(k) / heads]) + 15) & ~15;
         const int s = k % C::V_ST;
-        const uint32_t idesc = idesc_f16kind(128, 64, fmt) | (1u << 16);  // B MN-major
+        // B = V is MN-major (keys x head dims). MODE 3 issues Ph·[Vh | Vl] as one
+        // N=128 MMA (Vh and Vl tiles 16 KB apart = the MN-direction atom stride)
+        // into O columns [0,64) | [64,128), plus Pl·Vh into [0,64):
+        // 2 A-from-TMEM MMAs per 16 keys instead of 3.
+        const uint32_t idesc64 = idesc_f16kind(128, 64, fmt) | (1u << 16);
+        const uint32_t idesc128 = idesc_f16kind(128, 128, fmt) | (1u << 16);
         uint8_t* t = sm + C::QK_ST * C::QK_BYTES + s * C::V_BYTES;
-        const uint32_t tp = tm + b * 128, to = tm + 256 + b * 64;
+        const uint32_t tp = tm + b * 128, to = tm + 256 + b * 128;
         for (int kk = 0; kk < n16; kk += 16) {
           const uint32_t ph_ = tp + 32 * (kk >> 5) + 8 * ((kk >> 4) & 1);
           const uint64_t vh = umma_desc_sw128(t + kk * 128);
-          tc_mma_ts(to, ph_, vh, idesc, kk != 0);
-          if (PSPLIT) tc_mma_ts(to, ph_ + 16, vh, idesc, 1);
-          if (SPLIT) {
-            const uint64_t vl = umma_desc_sw128(t + ATQ_TILE + kk * 128);
-            tc_mma_ts(to, ph_, vl, idesc, 1);
-          }
+          if (SPLIT)
+            tc_mma_ts(to, ph_, umma_desc_sw128_mn(t + kk * 128, ATQ_TILE), idesc128, kk != 0);
+          else
+            tc_mma_ts(to, ph_, vh, idesc64, kk != 0);
+          if (PSPLIT) tc_mma_ts(to, ph_ + 16, vh, idesc64, 1);
         }
         tc_commit(&o_full[b]);
-        tc_commit(&v_empty[s]);
       };
       int ks = 0, ko = 0;
       const long long t0 = clock64();
@@ -289,84 +306,89 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
     const int r = q * 32 + lane;            // tile row owned by this thread
     const int pair_bar = 1 + g * 4 + q;     // named barrier of the two warps of this quarter
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const uint32_t tmax = tm + lane_off + 384 + 4 * g;
+    float* red_max = reinterpret_cast<float*>(sm + C::RED_OFF) + g * 512;  // [half][row]
+    float* red_sum = red_max + 256;
     const float c2 = scale * 1.4426950408889634f;  // exp(x*scale) = 2^(x*c2)
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
     for (int k = g; k < mine; k += 2) {
       const int b = g;
       const int it = item_of(k);
       const AttTile tl = tiles[it / heads];
       const int h = it % heads;
-      const int n = att_tile_rows(tl), n16 = (n + 15) & ~15;
-      // this row's sequence: keys [ks, ke) of the tile, token index tok
-      int ks = 0, ke = 0, tok = -1;
+      const int n16 = (att_tile_rows(tl) + 15) & ~15;
+      // The 32 rows of this warp are one 32-row granule, i.e. (part of) exactly
+      // one sequence slot: its keys are [ks, ke) of the tile (warp-uniform).
+      int ks = 0, ke = 0, t0 = 0;
       {
         int o = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int L = tl.len[j], R = (L + 31) & ~31;
-          if (r >= o && r < o + R) {
-            if (r - o < L) {
-              ks = o;
-              ke = o + L;
-              tok = tl.t0[j] + (r - o);
-            }
+          if (q * 32 >= o && q * 32 < o + R) {
+            ks = o;
+            ke = o + L;
+            t0 = tl.t0[j];
           }
           o += R;
         }
       }
+      const bool active = ke > ks;
       mbar_wait(&s_full[b], (k >> 1) & 1);
       const bool tr = hf == 0 && q == 0 && lane == 0;
       if (tr) ATT_TRACE(k, 2);
       tc_fence_after();
-      const bool active = q * 32 < n;  // warp-uniform (same for both warps of the pair)
-      float sum = 1.f;
       if (active) {
         const uint32_t trow = tm + b * 128 + lane_off;
-        int lo = tok >= 0 ? ks : 1 << 20, hi = tok >= 0 ? ke : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-          hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        }
-        const int c_lo = lo >> 5, c_hi = (hi - 1) >> 5, c_end = (n16 + 31) >> 5;
-        const bool use[2] = {hf >= c_lo && hf <= c_hi, hf + 2 >= c_lo && hf + 2 <= c_hi};
+        const int c_lo = ks >> 5, c_hi = (ke - 1) >> 5, c_end = (n16 + 31) >> 5;
         float mx = -INFINITY;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          if (use[j]) {
+          const int c = hf + 2 * j;
+          if (c >= c_lo && c <= c_hi) {
             float v[32];
-            tmem_ld_32x32(trow + (hf + 2 * j) * 32, v);
-            const int a = ks - (hf + 2 * j) * 32, e = ke - (hf + 2 * j) * 32;
+            tmem_ld_32x32(trow + c * 32, v);
+            const int e = ke - c * 32;  // keys i < e of this chunk are the sequence's
+            if (e >= 32) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (i >= a && i < e) mx = fmaxf(mx, v[i]);
+              for (int i = 0; i < 32; ++i) mx = fmaxf(mx, v[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (i < e) mx = fmaxf(mx, v[i]);
+            }
           }
         }
-        tmem_st_1(tmax + hf, __float_as_uint(mx));
-        tc_wait_st();
-        tc_fence_before();
-        asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-        tc_fence_after();
-        mx = fmaxf(mx, tmem_ld_1(tmax + (hf ^ 1)));
+        red_max[hf * 128 + r] = mx;
+        pair_sync();
+        mx = fmaxf(mx, red_max[(hf ^ 1) * 128 + r]);
         const float mxc = mx * c2;
-        sum = 0.f;
+        float sum = 0.f;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int c = hf + 2 * j;
           if (c < c_end) {
+            const bool in = c >= c_lo && c <= c_hi;
+            const int e = ke - c * 32;
             float v[32];
-            if (use[j]) tmem_ld_32x32(trow + c * 32, v);
+            if (in) tmem_ld_32x32(trow + c * 32, v);
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
               uint32_t hh[8], ll[8];
-              if (use[j]) {
-                const int a = ks - c * 32 - half * 16, e = ke - c * 32 - half * 16;
+              if (in && e >= 32) {
 #pragma unroll
                 for (int i = 0; i < 16; i += 2) {
-                  const float x0 = v[half * 16 + i], x1 = v[half * 16 + i + 1];
-                  const float p0 = (i >= a && i < e) ? fast_exp2(fmaf(x0, c2, -mxc)) : 0.f;
+                  const float p0 = fast_exp2(fmaf(v[half * 16 + i], c2, -mxc));
+                  const float p1 = fast_exp2(fmaf(v[half * 16 + i + 1], c2, -mxc));
+                  sum += p0 + p1;
+                  split2(p0, p1, fmt, hh[i / 2], ll[i / 2]);
+                }
+              } else if (in) {
+                const int eh = e - half * 16;
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) {
+                  const float p0 = i < eh ? fast_exp2(fmaf(v[half * 16 + i], c2, -mxc)) : 0.f;
                   const float p1 =
-                      (i + 1 >= a && i + 1 < e) ? fast_exp2(fmaf(x1, c2, -mxc)) : 0.f;
+                      i + 1 < eh ? fast_exp2(fmaf(v[half * 16 + i + 1], c2, -mxc)) : 0.f;
                   sum += p0 + p1;
                   split2(p0, p1, fmt, hh[i / 2], ll[i / 2]);
                 }
@@ -379,12 +401,9 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
             }
           }
         }
-      }
-      if (active) {
-        tmem_st_1(tmax + 2 + hf, __float_as_uint(sum));
         tc_wait_st();
-        tc_fence_before();
-        asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+        red_sum[hf * 128 + r] = sum;
+        pair_sync();
       }
       tc_fence_before();
       mbar_arrive(&p_full[b]);
@@ -394,25 +413,54 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
       if (tr) ATT_TRACE(k, 4);
       tc_fence_after();
       if (active) {
-        float v[32];
-        tmem_ld_32x32(tm + lane_off + 256 + b * 64 + hf * 32, v);
-        const float inv = 1.0f / (tmem_ld_1(tmax + 2) + tmem_ld_1(tmax + 3));
-        if (tok >= 0) {
-          // ctx is a convex combination of range-checked V rows: no fp16 overflow possible
-          const size_t ob = (size_t)tok * ldc + h * 64 + hf * 32;
-          uint32_t hh[16], ll[16];
+        const uint32_t to = tm + lane_off + 256 + b * 128 + hf * 32;
+        const float inv = 1.0f / (red_sum[r] + red_sum[128 + r]);
+        // Stage ctx rows in this item's V stage (the O MMAs finished reading V)
+        // as [row][128 B] per plane, 16-byte chunks XOR-swizzled by row, then
+        // each warp of the pair writes 16 whole 128-byte rows per plane.
+        uint8_t* stg = sm + C::QK_ST * C::QK_BYTES + (k % C::V_ST) * C::V_BYTES;
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) split2(v[i] * inv, v[i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
+        for (int half = 0; half < 2; ++half) {
+          float v[16];
+          tmem_ld_32x16(to + half * 16, v);
+          if (SPLIT) {  // O = Ph·Vh + Pl·Vh (columns 0..63) + Ph·Vl (64..127)
+            float w[16];
+            tmem_ld_32x16(to + 64 + half * 16, w);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            *reinterpret_cast<uint4*>(ch + ob + 8 * u) =
+            for (int i = 0; i < 16; ++i) v[i] += w[i];
+          }
+          // ctx is a convex combination of range-checked V rows: no fp16 overflow
+          uint32_t hh[8], ll[8];
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) split2(v[i] * inv, v[i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int chunk = hf * 4 + half * 2 + u;
+            const uint32_t off = r * 128 + ((chunk ^ (r & 7)) << 4);
+            *reinterpret_cast<uint4*>(stg + off) =
                 make_uint4(hh[4 * u], hh[4 * u + 1], hh[4 * u + 2], hh[4 * u + 3]);
             if (SPLIT)
-              *reinterpret_cast<uint4*>(cl + ob + 8 * u) =
+              *reinterpret_cast<uint4*>(stg + ATQ_TILE + off) =
                   make_uint4(ll[4 * u], ll[4 * u + 1], ll[4 * u + 2], ll[4 * u + 3]);
           }
         }
+        pair_sync();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int row = q * 32 + hf * 16 + i * 4 + (lane >> 3), chunk = lane & 7;
+          if (row < ke) {
+            const uint32_t off = row * 128 + ((chunk ^ (row & 7)) << 4);
+            const size_t o = (size_t)(t0 + row - ks) * ldc + h * 64 + chunk * 8;
+            *reinterpret_cast<uint4*>(ch + o) = *reinterpret_cast<const uint4*>(stg + off);
+            if (SPLIT)
+              *reinterpret_cast<uint4*>(cl + o) = *reinterpret_cast<const uint4*>(stg + ATQ_TILE + off);
+          }
+        }
       }
+      // generic-proxy staging traffic before the stage's next TMA (async proxy) fill
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&v_empty[k % C::V_ST]);
       tc_fence_before();
       if (tr) ATT_TRACE(k, 5);
     }

@@ -130,9 +130,15 @@ static cudaError_t run_epi(int epi, const CUtensorMap* ah, const CUtensorMap* al
 }
 
 cudaError_t launch_gemm(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* bh,
-                        const CUtensorMap* bl, int bn, int nsplit, int epi, const GemmArgs& a,
+                        const CUtensorMap* bl, int bn, int nsplit, int epi, const GemmArgs& a_in,
                         int num_sms, cudaStream_t st) {
-  if (a.K % GEMM_BK != 0 || a.N % bn != 0) return cudaErrorInvalidValue;
+  if (a_in.K % GEMM_BK != 0 || a_in.N % bn != 0) return cudaErrorInvalidValue;
+  static const int group_m = [] {
+    const char* e = getenv("MFG_GEMM_GROUP");
+    return e ? atoi(e) : 0;
+  }();
+  GemmArgs a = a_in;
+  a.group_m = group_m;
   const bool split = nsplit == 2;
   if (gemm_uses_pair(bn))
     return split ? run2_epi<true>(epi, ah, al, bh, bl, a, num_sms, st)

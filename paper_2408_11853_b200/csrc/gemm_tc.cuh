@@ -46,12 +46,31 @@ struct GemmArgs {
   int ldh;
   int fmt;                   // FMT_F16 / FMT_BF16: operand format of A, B and out_hi/lo
   int* ovf;                  // set to 1 when an fp16 output overflows
+  int group_m;               // tile raster: blocks of group_m M-tiles walk M fastest (0: N fastest)
   int r16;                   // reference binary16 mode (`encoder.py:120-126`): round the
                              // product to fp16, add the fp16 bias in fp16, round residual
                              // sums to fp16 (bias must hold fp16-representable values)
 };
 
 __device__ __forceinline__ float round16(float v) { return __half2float(__float2half_rn(v)); }
+
+// Tile index -> (m block, n block). group_m > 0: groups of group_m M-blocks
+// walk M fastest, so the CTAs running at the same time share each weight
+// (B) tile and re-read each activation (A) block while it is still in L2.
+__device__ __forceinline__ void tile_mn(int tile, int num_m, int num_n, int group_m, int& m,
+                                        int& n) {
+  if (group_m <= 0) {
+    m = tile / num_n;
+    n = tile % num_n;
+    return;
+  }
+  const int per = group_m * num_n;
+  const int first = (tile / per) * group_m;
+  const int gs = min(group_m, num_m - first);
+  const int in = tile % per;
+  m = first + in % gs;
+  n = in / gs;
+}
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
@@ -211,8 +230,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int m0 = (tile / num_n) * GEMM_BM;
-        const int n0 = (tile % num_n) * BN;
+        int mt, nt;
+        tile_mn(tile, num_m, num_n, args.group_m, mt, nt);
+        const int m0 = mt * GEMM_BM;
+        const int n0 = nt * BN;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], C::STAGE_BYTES);
@@ -276,8 +297,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      const int m0 = (tile / num_n) * GEMM_BM;
-      const int n0 = (tile % num_n) * BN;
+      int mt, nt;
+      tile_mn(tile, num_m, num_n, args.group_m, mt, nt);
+      const int m0 = mt * GEMM_BM;
+      const int n0 = nt * BN;
       const int row0 = m0 + q * 32;
       const int rows = min(32, args.M - row0);
       mbar_wait(&tfull[acc], acc_phase);
@@ -387,8 +410,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = pair; tile < tiles; tile += npairs) {
-        const int m0 = (tile / num_n) * 2 * GEMM_BM + rank * GEMM_BM;
-        const int n0 = (tile % num_n) * BN + rank * 128;
+        int mt, nt;
+        tile_mn(tile, num_m, num_n, args.group_m, mt, nt);
+        const int m0 = mt * 2 * GEMM_BM + rank * GEMM_BM;
+        const int n0 = nt * BN + rank * 128;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
@@ -461,8 +486,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = pair; tile < tiles; tile += npairs) {
-      const int m0 = (tile / num_n) * 2 * GEMM_BM + rank * GEMM_BM;
-      const int n0 = (tile % num_n) * BN;
+      int mt, nt;
+      tile_mn(tile, num_m, num_n, args.group_m, mt, nt);
+      const int m0 = mt * 2 * GEMM_BM + rank * GEMM_BM;
+      const int n0 = nt * BN;
       const int row0 = m0 + q * 32;
       const int rows = min(32, args.M - row0);
       mbar_wait(&tfull[acc], acc_phase);

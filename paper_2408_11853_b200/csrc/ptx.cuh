@@ -218,6 +218,19 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(const void* smem_tile) {
   return d;
 }
 
+// MN-major operand with 128-byte swizzle whose N extent spans several 64-element
+// atoms: atoms `atom_stride` bytes apart (LBO), 8-row K groups 1024 bytes apart (SBO).
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(const void* smem_tile, uint32_t atom_stride) {
+  const uint64_t addr = smem_u32(smem_tile);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;
+  d |= (uint64_t)((atom_stride >> 4) & 0x3FFF) << 16;  // LBO
+  d |= (uint64_t)(1024 >> 4) << 32;                    // SBO
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
 // Instruction descriptor, kind::f16 -> fp32 accumulate, both operands K-major.
 // fmt: FMT_F16 (0) or FMT_BF16 (1) for both A and B.
 __host__ __device__ constexpr uint32_t idesc_f16kind(uint32_t M, uint32_t N, uint32_t fmt) {

@@ -81,11 +81,11 @@ def launch_list(path):
 def main(rep, launches, tag):
     kernels = full_set(rep)
     shares, total_ms = launch_list(launches)
-    gemms = [k for k in kernels if k["kernel"].startswith("gemm_tc_kernel")]
+    gemms = [k for k in kernels if k["kernel"].startswith(("gemm_tc_kernel", "gemm2_tc_kernel"))]
     dom = max(gemms, key=lambda k: k.get("duration_ms", 0)) if gemms else None
     summary = {
         "tag": tag,
-        "how": "ncu --set full --clock-control none (1 window of 1024 config-2 records, "
+        "how": "ncu --set full --clock-control none (first layer of 1 window of 1024 config-2 records, "
                "tools/profile_window.py); launch list: ncu --metrics gpu__time_duration.sum",
         "window_total_ms_serialised": total_ms,
         "launch_shares": shares,
