@@ -37,8 +37,10 @@ enum EpiMode : int {
 struct GemmArgs {
   int M, N, K;               // M real rows; N, K padded (N % BN == 0, K % 64 == 0)
   const float* bias;         // [N]
-  const float* residual;     // [M][ldr] (EPI_F32_RES)
+  const float* residual;     // [M][ldr] (EPI_F32_RES), fp32 ...
   int ldr;
+  const uint16_t* res_hi;    // ... or, when non-null, 16-bit hi (+ lo) pieces [M][ldr]
+  const uint16_t* res_lo;    //     in `fmt` (residual stream kept as operand pieces)
   float* out_f32;            // [M][ldo] (EPI_F32*)
   int ldo;
   uint16_t* out_hi;          // [M][ldh] (split epilogues), 16-bit pieces in `fmt`
@@ -109,15 +111,22 @@ __device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, in
 #pragma unroll 1
   for (int c = half * 32; c < BN; c += 64) {
     const int col = n0 + c + 4 * cg;
-    // prefetch this chunk's residual (8 x float4 per lane) before touching TMEM
+    // prefetch this chunk's residual (8 x float4, or 8 x (hi, lo) 4 x 16-bit
+    // pieces per lane) before touching TMEM; converted where it is consumed
     float4 res[8];
+    uint2 rh[8], rl[8];
+    const bool r16res = EPI == EPI_F32_RES && args.res_hi != nullptr;
     if (EPI == EPI_F32_RES) {
 #pragma unroll
       for (int it = 0; it < 8; ++it) {
         const int r = it * 4 + rs;
-        res[it] = r < rows ? *reinterpret_cast<const float4*>(
-                                 args.residual + (size_t)(row0 + r) * args.ldr + col)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        const size_t o = (size_t)(row0 + (r < rows ? r : 0)) * args.ldr + col;
+        if (r16res) {
+          rh[it] = *reinterpret_cast<const uint2*>(args.res_hi + o);
+          rl[it] = args.res_lo ? *reinterpret_cast<const uint2*>(args.res_lo + o) : make_uint2(0u, 0u);
+        } else {
+          res[it] = *reinterpret_cast<const float4*>(args.residual + o);
+        }
       }
     }
     float v[32];
@@ -141,6 +150,14 @@ __device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, in
         const size_t o = (size_t)(row0 + r);
         if (EPI == EPI_F32 || EPI == EPI_F32_RES) {
           if (EPI == EPI_F32_RES) {
+            if (r16res) {
+              const uint16_t* h = reinterpret_cast<const uint16_t*>(&rh[it]);
+              const uint16_t* l = reinterpret_cast<const uint16_t*>(&rl[it]);
+              res[it] = make_float4(load16(h, 0, args.fmt) + load16(l, 0, args.fmt),
+                                    load16(h, 1, args.fmt) + load16(l, 1, args.fmt),
+                                    load16(h, 2, args.fmt) + load16(l, 2, args.fmt),
+                                    load16(h, 3, args.fmt) + load16(l, 3, args.fmt));
+            }
             x[0] += res[it].x; x[1] += res[it].y; x[2] += res[it].z; x[3] += res[it].w;
             if (args.r16) {
               x[0] = round16(x[0]); x[1] = round16(x[1]); x[2] = round16(x[2]); x[3] = round16(x[3]);

@@ -31,7 +31,7 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __r
     for (int c = lane; c < d; c += 32) {
       float v = a[c] + b[c];
       if (r16) v = __half2float(__float2half_rn(v));  // binary16 add (reference fp16 mode)
-      x32[o + c] = v;
+      if (x32) x32[o + c] = v;
       if (xh) store_split(xh, xl, o + c, v, fmt, flag);
     }
   }

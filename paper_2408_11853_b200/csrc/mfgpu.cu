@@ -371,7 +371,7 @@ struct mfg_ctx {
 
   // ---------------------------------------------------------------- forward
   void gemm(const Act& a, const Weight& w, int M, int epi, int cls, const float* res, int ldr,
-            float* out32, int ldo, Act* outa) {
+            float* out32, int ldo, Act* outa, const Act* res16 = nullptr) {
     GemmArgs g{};
     g.M = M;
     g.N = w.Npad;
@@ -379,6 +379,11 @@ struct mfg_ctx {
     g.bias = w.bias;
     g.residual = res;
     g.ldr = ldr;
+    if (res16) {
+      g.res_hi = res16->hi;
+      g.res_lo = res16->lo;
+      g.ldr = res16->ld;
+    }
     g.out_f32 = out32;
     g.ldo = ldo;
     g.fmt = fmt;
@@ -419,11 +424,20 @@ struct mfg_ctx {
     const int Ti = (int)T;
     {
       int e = ev_begin();
-      CK(launch_embed(d_ids, d_cu, nseq, (int)man.vocab_size, d, tok, pos, x32, dp,
-                      pre_norm ? nullptr : xa.hi, pre_norm ? nullptr : xa.lo, fmt, r16, d_ovf, st));
-      ev_end(e, C_EMB, 0, (double)T * d * (8 + 4 + (pre_norm ? 0 : (split ? 4 : 2))));
+      // post-norm with split (or exact binary16) operands: the residual stream
+      // lives only in the operand pieces xa (hi + lo ~ 22 bits), so LayerNorm
+      // writes 8 instead of 12 bytes per element; x32 is written once, by the
+      // last LayerNorm, for pooling
+      const bool res16 = !pre_norm && (split || r16);
+      CK(launch_embed(d_ids, d_cu, nseq, (int)man.vocab_size, d, tok, pos, res16 ? nullptr : x32,
+                      dp, pre_norm ? nullptr : xa.hi, pre_norm ? nullptr : xa.lo, fmt, r16, d_ovf,
+                      st));
+      ev_end(e, C_EMB, 0, (double)T * d * (8 + (res16 ? 0 : 4) + (pre_norm ? 0 : (split ? 4 : 2))));
     }
-    for (auto& L : layers) {
+    const bool res16 = !pre_norm && (split || r16);
+    for (size_t li = 0; li < layers.size(); ++li) {
+      Layer& L = layers[li];
+      const bool last = li + 1 == layers.size();
       if (pre_norm) layernorm(x32, Ti, L.g1, L.b1, nullptr, &xa);
       gemm(xa, L.qkv, Ti, EPI_SPLIT, C_QKV, nullptr, 0, nullptr, 0, &qa);
       {
@@ -438,13 +452,14 @@ struct mfg_ctx {
         ev_end(e, C_ATT, 4.0 * sum_l2 * d, bytes);
         if (n_tiles > 0 && n_work > 0) stats.kernel_launches += 1;
       }
-      gemm(ca, L.o, Ti, EPI_F32_RES, C_O, x32, dp, y32, dp, nullptr);
       if (!pre_norm) {
-        layernorm(y32, Ti, L.g1, L.b1, x32, &xa);
+        gemm(ca, L.o, Ti, EPI_F32_RES, C_O, x32, dp, y32, dp, nullptr, res16 ? &xa : nullptr);
+        layernorm(y32, Ti, L.g1, L.b1, res16 ? nullptr : x32, &xa);
         gemm(xa, L.w1, Ti, EPI_GELU_SPLIT, C_FFN1, nullptr, 0, nullptr, 0, &ha);
-        gemm(ha, L.w2, Ti, EPI_F32_RES, C_FFN2, x32, dp, y32, dp, nullptr);
-        layernorm(y32, Ti, L.g2, L.b2, x32, &xa);
+        gemm(ha, L.w2, Ti, EPI_F32_RES, C_FFN2, x32, dp, y32, dp, nullptr, res16 ? &xa : nullptr);
+        layernorm(y32, Ti, L.g2, L.b2, (res16 && !last) ? nullptr : x32, &xa);
       } else {
+        gemm(ca, L.o, Ti, EPI_F32_RES, C_O, x32, dp, y32, dp, nullptr);
         layernorm(y32, Ti, L.g2, L.b2, nullptr, &xa);
         gemm(xa, L.w1, Ti, EPI_GELU_SPLIT, C_FFN1, nullptr, 0, nullptr, 0, &ha);
         gemm(ha, L.w2, Ti, EPI_F32_RES, C_FFN2, y32, dp, x32, dp, nullptr);
