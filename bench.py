@@ -280,8 +280,11 @@ def run_ours(args, rank, world, local_rank):
     lines = workload_lines(args.config, R * n_steps, fx.TEXT_SEED + 1000 * rank)
 
     # ---------------- device-resident timing (value)
+    t_load = time.perf_counter()
     model = mf.GpuScoringModel(path, device=local_rank, precision=args.precision,
                                profile=True)
+    torch.cuda.synchronize()
+    load_s = time.perf_counter() - t_load
     vocab = mf.load_vocab(vocab_path)
     kind = mf.Kind.parse(man["like"])
     max_len = min(512, man["max_position"])
@@ -425,6 +428,7 @@ def run_ours(args, rank, world, local_rank):
                 "path": "Evaluator.evaluate_lines (host TSV -> libmfhost -> libmfgpu -> scores)"},
         "gpu_launches": int(stats["kernel_launches"]),
         "other_precisions": others,
+        "model_load_s": load_s,
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:

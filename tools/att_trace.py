@@ -39,3 +39,18 @@ print("mean per-item deltas (cycles): S_seen-S_iss %.0f, P_done-S_seen %.0f, O_i
           (d_[..., 2] - d_[..., 0]).mean(), (d_[..., 3] - d_[..., 2]).mean(),
           (d_[..., 1] - d_[..., 3]).mean(), (d_[..., 4] - d_[..., 1]).mean(),
           (d_[..., 5] - d_[..., 4]).mean(), np.diff(tr[:, 4:60, 0], axis=1).mean()))
+
+# wall time of the same launch (CUDA events around mfgt_attention's kernel are not
+# exposed; time the whole call minus its H2D by repeating it)
+import time
+import torch
+lib.mfgt_attention(0, len(lens), cu.ctypes.data_as(C.POINTER(C.c_int32)), d, H, P(qkv), P(out), 1)
+t0 = time.perf_counter()
+for _ in range(5):
+    lib.mfgt_attention(0, len(lens), cu.ctypes.data_as(C.POINTER(C.c_int32)), d, H, P(qkv), P(out), 1)
+print("mfgt_attention call (incl. H2D/D2H of %.0f MB): %.2f ms" % (qkv.nbytes / 1e6, (time.perf_counter() - t0) / 5 * 1e3))
+starts = tr[:, :, 0]
+ends = tr[:, :, 5]
+for cta in range(4):
+    n = int((tr[cta, :, 0] > 0).sum())
+    print(f"CTA {cta}: {n} traced items, first S issue -> last epilogue {ends[cta, n-1] - starts[cta, 0]} cycles")
