@@ -138,14 +138,18 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
-def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+def ncu_traffic(cls=None):
+    """dram bytes per launch of kernel class `cls` (else the dominant GEMM) from the
+    newest committed ncu summary (profiles/ncu_summary_*.json)."""
     for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True) \
             if os.path.isdir(os.path.join(ROOT, "profiles")) else []:
         if name.startswith("ncu_summary") and name.endswith(".json"):
             try:
                 with open(os.path.join(ROOT, "profiles", name)) as f:
-                    return json.load(f).get("dram_bytes_per_launch"), name
+                    summ = json.load(f)
+                if cls and cls in summ.get("by_class", {}):
+                    return summ["by_class"][cls]["dram_bytes"], name
+                return summ.get("dram_bytes_per_launch"), name
             except Exception:
                 pass
     return None, None
@@ -383,7 +387,7 @@ def run_ours(args, rank, world, local_rank):
     achieved = (c["flops"] / max(1, c["launches"])) / (per_launch_ms / 1e3) / 1e12
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
     mma_per_step = 1 if args.precision in ("bf16", "fp16") else 3
-    traffic, traffic_src = ncu_traffic()
+    traffic, traffic_src = ncu_traffic(dom)
     gemm_ms = sum(cls[k]["ms"] for k in gemm_names)
     gemm_flops = sum(cls[k]["flops"] for k in gemm_names)
     all_ms = sum(v["ms"] for v in cls.values())
@@ -401,7 +405,14 @@ def run_ours(args, rank, world, local_rank):
         "traffic_source": traffic_src,
     }
     if cls["attention"]["ms"]:
-        roofline["attention_tflops_fp32_simt"] = cls["attention"]["flops"] / (cls["attention"]["ms"] / 1e3) / 1e12
+        gbs = cls["attention"]["bytes"] / (cls["attention"]["ms"] / 1e3) / 1e9
+        att_traffic, _ = ncu_traffic("attention")
+        roofline["attention_hbm"] = {
+            "achieved_gbs": gbs, "peak_gbs": peaks.get("hbm_gbs"),
+            "frac": gbs / peaks.get("hbm_gbs", 6544.3),
+            "algorithmic_bytes_per_launch": cls["attention"]["bytes"] / max(1, cls["attention"]["launches"]),
+            "traffic": att_traffic,
+            "tflops": cls["attention"]["flops"] / (cls["attention"]["ms"] / 1e3) / 1e12}
     if cls["layernorm"]["ms"]:
         gbs = cls["layernorm"]["bytes"] / (cls["layernorm"]["ms"] / 1e3) / 1e9
         roofline["layernorm_hbm"] = {"achieved_gbs": gbs, "peak_gbs": peaks.get("hbm_gbs"),

@@ -93,6 +93,12 @@ def main(rep, launches, tag):
         "dominant_gemm": dom,
         "dram_bytes_per_launch": (dom["dram_read_bytes"] + dom["dram_write_bytes"]) if dom else None,
     }
+    # the full-set capture is layer 0 of the window in launch order
+    order = ["qkv", "attention", "o_proj", "layernorm", "ffn1", "ffn2"]
+    if len(kernels) >= len(order):
+        summary["by_class"] = {c: dict(kernels[i], dram_bytes=kernels[i].get("dram_read_bytes", 0)
+                                       + kernels[i].get("dram_write_bytes", 0))
+                               for i, c in enumerate(order)}
     os.makedirs("profiles", exist_ok=True)
     dst = os.path.join("profiles", f"ncu_summary_{tag}.json")
     with open(dst, "w") as f:
