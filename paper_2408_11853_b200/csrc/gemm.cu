@@ -96,7 +96,7 @@ static cudaError_t run2(const CUtensorMap* ah, const CUtensorMap* al, const CUte
   const int tiles = ((a.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * (a.N / 256);
   if (tiles <= 0) return cudaSuccess;
   const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  kern<<<2 * pairs, GEMM_THREADS, C::SMEM_BYTES, st>>>(*ah, SPLIT ? *al : *ah, *bh,
+  kern<<<2 * pairs, C::THREADS, C::SMEM_BYTES, st>>>(*ah, SPLIT ? *al : *ah, *bh,
                                                        SPLIT ? *bl : *bh, a);
   return cudaGetLastError();
 }

@@ -103,18 +103,17 @@ struct GemmCfg {
 // row0..row0+rows-1 (this warp's quarter), every other 32-column chunk starting
 // at `half`*32; each chunk transposed through `buf` so global traffic is float4
 // per lane, 4 full 128-byte row segments per warp instruction.
-template <int BN, int EPI>
+template <int BN, int EPI, int NSUB = 2>
 __device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, int row0, int rows,
                                          int n0, int half, float* buf, int lane) {
   const int cg = lane & 7;       // transposed phase: 4 columns 4*cg..4*cg+3
   const int rs = lane >> 3;      // row sub-index 0..3
 #pragma unroll 1
-  for (int c = half * 32; c < BN; c += 64) {
+  for (int c = half * 32; c < BN; c += 32 * NSUB) {
     const int col = n0 + c + 4 * cg;
     // prefetch this chunk's residual (8 x float4, or 8 x (hi, lo) 4 x 16-bit
     // pieces per lane) before touching TMEM; converted where it is consumed
-    float4 res[8];
-    uint2 rh[8], rl[8];
+    uint4 rraw[8];  // float4 bits, or {hi pieces x2, lo pieces x2}
     const bool r16res = EPI == EPI_F32_RES && args.res_hi != nullptr;
     if (EPI == EPI_F32_RES) {
 #pragma unroll
@@ -122,10 +121,12 @@ __device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, in
         const int r = it * 4 + rs;
         const size_t o = (size_t)(row0 + (r < rows ? r : 0)) * args.ldr + col;
         if (r16res) {
-          rh[it] = *reinterpret_cast<const uint2*>(args.res_hi + o);
-          rl[it] = args.res_lo ? *reinterpret_cast<const uint2*>(args.res_lo + o) : make_uint2(0u, 0u);
+          const uint2 h = *reinterpret_cast<const uint2*>(args.res_hi + o);
+          const uint2 l = args.res_lo ? *reinterpret_cast<const uint2*>(args.res_lo + o)
+                                      : make_uint2(0u, 0u);
+          rraw[it] = make_uint4(h.x, h.y, l.x, l.y);
         } else {
-          res[it] = *reinterpret_cast<const float4*>(args.residual + o);
+          rraw[it] = *reinterpret_cast<const uint4*>(args.residual + o);
         }
       }
     }
@@ -150,15 +151,19 @@ __device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, in
         const size_t o = (size_t)(row0 + r);
         if (EPI == EPI_F32 || EPI == EPI_F32_RES) {
           if (EPI == EPI_F32_RES) {
+            float4 res;
             if (r16res) {
-              const uint16_t* h = reinterpret_cast<const uint16_t*>(&rh[it]);
-              const uint16_t* l = reinterpret_cast<const uint16_t*>(&rl[it]);
-              res[it] = make_float4(load16(h, 0, args.fmt) + load16(l, 0, args.fmt),
-                                    load16(h, 1, args.fmt) + load16(l, 1, args.fmt),
-                                    load16(h, 2, args.fmt) + load16(l, 2, args.fmt),
-                                    load16(h, 3, args.fmt) + load16(l, 3, args.fmt));
+              const uint16_t* h = reinterpret_cast<const uint16_t*>(&rraw[it].x);
+              const uint16_t* l = reinterpret_cast<const uint16_t*>(&rraw[it].z);
+              res = make_float4(load16(h, 0, args.fmt) + load16(l, 0, args.fmt),
+                                load16(h, 1, args.fmt) + load16(l, 1, args.fmt),
+                                load16(h, 2, args.fmt) + load16(l, 2, args.fmt),
+                                load16(h, 3, args.fmt) + load16(l, 3, args.fmt));
+            } else {
+              res = make_float4(__uint_as_float(rraw[it].x), __uint_as_float(rraw[it].y),
+                                __uint_as_float(rraw[it].z), __uint_as_float(rraw[it].w));
             }
-            x[0] += res[it].x; x[1] += res[it].y; x[2] += res[it].z; x[3] += res[it].w;
+            x[0] += res.x; x[1] += res.y; x[2] += res.z; x[3] += res.w;
             if (args.r16) {
               x[0] = round16(x[0]); x[1] = round16(x[1]); x[2] = round16(x[2]); x[3] = round16(x[3]);
             }
@@ -166,20 +171,31 @@ __device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, in
           *reinterpret_cast<float4*>(args.out_f32 + o * args.ldo + col) =
               make_float4(x[0], x[1], x[2], x[3]);
         } else {
-          uint16_t h[4], l[4];
-          bool ok = true;
+          float y[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float y = (EPI == EPI_GELU_SPLIT) ? gelu_tanh(x[j])
-                            : (EPI == EPI_TANH_SPLIT) ? tanhf(x[j]) : x[j];
-            ok &= split16(y, args.fmt, h[j], l[j]);
+          for (int j = 0; j < 4; ++j)
+            y[j] = (EPI == EPI_GELU_SPLIT) ? gelu_tanh(x[j])
+                   : (EPI == EPI_TANH_SPLIT) ? tanhf(x[j]) : x[j];
+          // fp16 range: |y| >= 65520 rounds to inf (binary16 overflow) -> flag
+          if (args.fmt == FMT_F16 && args.ovf &&
+              fmaxf(fmaxf(fabsf(y[0]), fabsf(y[1])), fmaxf(fabsf(y[2]), fabsf(y[3]))) >= 65520.f)
+            atomicOr(args.ovf, 1);
+          uint32_t h01, h23, l01, l23;
+          if (args.out_lo) {
+            split2(y[0], y[1], args.fmt, h01, l01);
+            split2(y[2], y[3], args.fmt, h23, l23);
+            *reinterpret_cast<uint2*>(args.out_lo + o * args.ldh + col) = make_uint2(l01, l23);
+          } else if (args.fmt == FMT_F16) {
+            const __half2 a = __floats2half2_rn(y[0], y[1]), c = __floats2half2_rn(y[2], y[3]);
+            h01 = *reinterpret_cast<const uint32_t*>(&a);
+            h23 = *reinterpret_cast<const uint32_t*>(&c);
+          } else {
+            const __nv_bfloat162 a = __floats2bfloat162_rn(y[0], y[1]),
+                                 c = __floats2bfloat162_rn(y[2], y[3]);
+            h01 = *reinterpret_cast<const uint32_t*>(&a);
+            h23 = *reinterpret_cast<const uint32_t*>(&c);
           }
-          if (!ok && args.ovf) atomicOr(args.ovf, 1);
-          *reinterpret_cast<uint2*>(args.out_hi + o * args.ldh + col) =
-              make_uint2(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16));
-          if (args.out_lo)
-            *reinterpret_cast<uint2*>(args.out_lo + o * args.ldh + col) =
-                make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
+          *reinterpret_cast<uint2*>(args.out_hi + o * args.ldh + col) = make_uint2(h01, h23);
         }
       }
     }
@@ -353,19 +369,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // tempty[a] lives in the leader and counts both CTAs' epilogue warps.
 template <bool SPLIT>
 struct Gemm2Cfg {
+  // one-MMA (non-split) tiles finish the mainloop 3x sooner, so their epilogue
+  // gets 16 warps (4 per TMEM lane quarter) instead of 8
+  static constexpr int EPI_WARPS = SPLIT ? 8 : 16;
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+  static constexpr int EPI_BYTES = EPI_WARPS * 32 * 33 * 4;
   static constexpr int NOPS = SPLIT ? 2 : 1;
   static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;  // this CTA's 128 rows
   static constexpr int B_BYTES = 128 * GEMM_BK * 2;      // this CTA's half of BN = 256
   static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
   static constexpr int STAGES_FIT =
-      (GEMM_SMEM_LIMIT - 1024 - GEMM_EPI_BYTES - GEMM_BAR_BYTES) / STAGE_BYTES;
+      (GEMM_SMEM_LIMIT - 1024 - EPI_BYTES - GEMM_BAR_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + GEMM_EPI_BYTES + GEMM_BAR_BYTES;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + GEMM_BAR_BYTES;
   static_assert(STAGES >= 2, "pipeline needs at least two stages");
 };
 
 template <bool SPLIT, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THREADS, 1)
     gemm2_tc_kernel(const __grid_constant__ CUtensorMap mapAh,
                     const __grid_constant__ CUtensorMap mapAl,
                     const __grid_constant__ CUtensorMap mapBh,
@@ -376,7 +397,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   float* epi_buf = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + GEMM_EPI_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -400,7 +421,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2 * GEMM_EPI_WARPS);
+      mbar_init(&tempty[a], 2 * C::EPI_WARPS);
     }
     fence_mbar_init();
   }
@@ -495,9 +516,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    const int ew = warp - 4;       // 0..7
+    const int ew = warp - 4;       // 0..EPI_WARPS-1
     const int q = warp & 3;        // TMEM lane quarter == 32-row block of this CTA's half tile
-    const int half = ew >> 2;      // which alternate 32-column chunks this warp owns
+    const int half = ew >> 2;      // which 32-column chunks (every EPI_WARPS/4-th) it owns
     float* buf = epi_buf + ew * 32 * 33;
     const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
     int acc = 0;
@@ -512,8 +533,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (rows > 0)
-        epi_tile<BN, EPI>(args, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, row0, rows, n0,
-                          half, buf, lane);
+        epi_tile<BN, EPI, C::EPI_WARPS / 4>(args, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN,
+                                            row0, rows, n0, half, buf, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
