@@ -309,9 +309,11 @@ __global__ void features_kernel(const float* __restrict__ x, int ld, int d, int 
                                 int fmt, int* ovf) {
   const int r = blockIdx.x;
   const size_t ro = (size_t)r * ldf;
-  const float* p0 = x + (size_t)cu[r] * ld;
-  const float* p1 = kind != 2 ? x + (size_t)cu[n + r] * ld : nullptr;
-  const float* p2 = kind == 1 ? x + (size_t)cu[2 * n + r] * ld : nullptr;
+  // cu == nullptr: x holds one (BOS) row per sequence, sequence-indexed
+  auto row = [&](int s) { return (size_t)(cu ? cu[s] : s) * ld; };
+  const float* p0 = x + row(r);
+  const float* p1 = kind != 2 ? x + row(n + r) : nullptr;
+  const float* p2 = kind == 1 ? x + row(2 * n + r) : nullptr;
   auto put = [&](int c, float v) { store_split(fh, fl, ro + c, v, fmt, ovf); };
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
     if (kind == 0) {
@@ -352,6 +354,22 @@ __global__ void transpose_split_kernel(const float* __restrict__ w, int K, int N
     const int n = n0 + i, k = k0 + threadIdx.x;
     if (n < N && k < K)
       store_split(hi, lo, (size_t)(row0 + n) * ldk + k, tile[threadIdx.x][i], fmt, ovf);
+  }
+}
+
+// BOS rows -> compact sequence-indexed rows (the last layer only feeds pooling,
+// `encoder.py:181-185`): dst row s = src row cu[s], for 16-bit planes and/or fp32.
+__global__ void gather_bos_kernel(const int32_t* __restrict__ cu, int d,
+                                  const uint16_t* __restrict__ sh, const uint16_t* __restrict__ sl,
+                                  int lds, const float* __restrict__ s32, int ld32,
+                                  uint16_t* __restrict__ dh, uint16_t* __restrict__ dl, int ldd,
+                                  float* __restrict__ d32, int ldd32) {
+  const int s = blockIdx.x;
+  const size_t src = (size_t)cu[s];
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    if (sh) dh[(size_t)s * ldd + c] = sh[src * lds + c];
+    if (sl) dl[(size_t)s * ldd + c] = sl[src * lds + c];
+    if (s32) d32[(size_t)s * ldd32 + c] = s32[src * ld32 + c];
   }
 }
 
@@ -435,6 +453,14 @@ cudaError_t launch_transpose_split(const float* w, int K, int N, uint16_t* hi, u
                                    int ldk, int row0, int fmt, int* ovf, cudaStream_t st) {
   dim3 grid((N + 31) / 32, (K + 31) / 32), block(32, 8);
   transpose_split_kernel<<<grid, block, 0, st>>>(w, K, N, hi, lo, ldk, row0, fmt, ovf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_bos(const int32_t* cu, int nseq, int d, const uint16_t* sh,
+                              const uint16_t* sl, int lds, const float* s32, int ld32, uint16_t* dh,
+                              uint16_t* dl, int ldd, float* d32, int ldd32, cudaStream_t st) {
+  if (nseq <= 0) return cudaSuccess;
+  gather_bos_kernel<<<nseq, 256, 0, st>>>(cu, d, sh, sl, lds, s32, ld32, dh, dl, ldd, d32, ldd32);
   return cudaGetLastError();
 }
 

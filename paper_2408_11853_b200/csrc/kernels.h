@@ -44,6 +44,10 @@ cudaError_t launch_features(const float* x, int ld, int d, int kind, const int32
                             cudaStream_t st);
 cudaError_t launch_transpose_split(const float* w, int K, int N, uint16_t* hi, uint16_t* lo,
                                    int ldk, int row0, int fmt, int* ovf, cudaStream_t st);
+// Copy the BOS row (cu[s]) of each sequence to compact row s (16-bit planes and/or fp32).
+cudaError_t launch_gather_bos(const int32_t* cu, int nseq, int d, const uint16_t* sh,
+                              const uint16_t* sl, int lds, const float* s32, int ld32, uint16_t* dh,
+                              uint16_t* dl, int ldd, float* d32, int ldd32, cudaStream_t st);
 cudaError_t launch_gather_col0(const float* out, int ld, int n, float* scores, cudaStream_t st);
 
 // ---- tcgen05 GEMM (gemm.cu)

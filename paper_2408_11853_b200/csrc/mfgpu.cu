@@ -95,6 +95,9 @@ struct mfg_ctx {
   int cap_records = 0;
   float *x32 = nullptr, *y32 = nullptr;
   Act xa, ca, ha, fa, qa;          // qa: Q|K|V pieces [T][qkv_ld]
+  // last layer on BOS rows only (one row per sequence): ctx, residual/LN, FFN hidden
+  Act cb, xb, hb;
+  float *x32b = nullptr, *y32b = nullptr;
   bool att_tc = false;              // tcgen05 attention usable (d_head == 64)
   AttTile *d_tiles = nullptr, *h_tiles = nullptr;  // attention tiles (att_plan_tiles)
   CUtensorMap qm32h{}, qm32l{};     // Q|K|V maps with 32-row boxes (attention tiles)
@@ -350,6 +353,14 @@ struct mfg_ctx {
     make_act(ca, cap_tokens, dp);
     make_act(ha, cap_tokens, fp);
     make_act(fa, cap_records, Fp);
+    {
+      const int64_t ns = (int64_t)cap_records * n_roles;
+      make_act(cb, ns, dp);
+      make_act(xb, ns, dp);
+      make_act(hb, ns, fp);
+      x32b = dalloc<float>((size_t)pad128(ns) * dp);
+      y32b = dalloc<float>((size_t)pad128(ns) * dp);
+    }
     ga.resize(head.size() - 1);
     for (size_t j = 0; j + 1 < head.size(); ++j) make_act(ga[j], cap_records, head[j].Npad);
     hout = dalloc<float>((size_t)pad128(cap_records) * head.back().Npad);
@@ -428,13 +439,13 @@ struct mfg_ctx {
       // lives only in the operand pieces xa (hi + lo ~ 22 bits), so LayerNorm
       // writes 8 instead of 12 bytes per element; x32 is written once, by the
       // last LayerNorm, for pooling
-      const bool res16 = !pre_norm && (split || r16);
+      const bool res16 = !pre_norm && (split || r16) && !layers.empty();
       CK(launch_embed(d_ids, d_cu, nseq, (int)man.vocab_size, d, tok, pos, res16 ? nullptr : x32,
                       dp, pre_norm ? nullptr : xa.hi, pre_norm ? nullptr : xa.lo, fmt, r16, d_ovf,
                       st));
       ev_end(e, C_EMB, 0, (double)T * d * (8 + (res16 ? 0 : 4) + (pre_norm ? 0 : (split ? 4 : 2))));
     }
-    const bool res16 = !pre_norm && (split || r16);
+    const bool res16 = !pre_norm && (split || r16) && !layers.empty();
     for (size_t li = 0; li < layers.size(); ++li) {
       Layer& L = layers[li];
       const bool last = li + 1 == layers.size();
@@ -452,12 +463,13 @@ struct mfg_ctx {
         ev_end(e, C_ATT, 4.0 * sum_l2 * d, bytes);
         if (n_tiles > 0 && n_work > 0) stats.kernel_launches += 1;
       }
+      if (last) break;  // the last layer's O-proj / FFN run on the BOS rows only (below)
       if (!pre_norm) {
         gemm(ca, L.o, Ti, EPI_F32_RES, C_O, x32, dp, y32, dp, nullptr, res16 ? &xa : nullptr);
         layernorm(y32, Ti, L.g1, L.b1, res16 ? nullptr : x32, &xa);
         gemm(xa, L.w1, Ti, EPI_GELU_SPLIT, C_FFN1, nullptr, 0, nullptr, 0, &ha);
         gemm(ha, L.w2, Ti, EPI_F32_RES, C_FFN2, x32, dp, y32, dp, nullptr, res16 ? &xa : nullptr);
-        layernorm(y32, Ti, L.g2, L.b2, (res16 && !last) ? nullptr : x32, &xa);
+        layernorm(y32, Ti, L.g2, L.b2, res16 ? nullptr : x32, &xa);
       } else {
         gemm(ca, L.o, Ti, EPI_F32_RES, C_O, x32, dp, y32, dp, nullptr);
         layernorm(y32, Ti, L.g2, L.b2, nullptr, &xa);
@@ -465,9 +477,40 @@ struct mfg_ctx {
         gemm(ha, L.w2, Ti, EPI_F32_RES, C_FFN2, y32, dp, x32, dp, nullptr);
       }
     }
+    // Last layer: pooling reads only the BOS row of every sequence (`encoder.py:181-185`)
+    // and rows are independent after attention, so the O-projection, both
+    // LayerNorms and the FFN run on one row per sequence (bitwise the same values).
+    if (!layers.empty()) {
+      Layer& L = layers.back();
+      const int S = nseq;
+      {
+        int e = ev_begin();
+        const bool res_pieces = res16;
+        CK(launch_gather_bos(d_cu, S, d, ca.hi, ca.lo, ca.ld, nullptr, 0, cb.hi, cb.lo, cb.ld,
+                             nullptr, 0, st));
+        CK(launch_gather_bos(d_cu, S, d, res_pieces ? xa.hi : nullptr,
+                             res_pieces ? xa.lo : nullptr, xa.ld, res_pieces ? nullptr : x32, dp,
+                             xb.hi, xb.lo, xb.ld, x32b, dp, st));
+        stats.kernel_launches += 1;
+        ev_end(e, C_HEAD, 0, (double)S * d * 16);
+      }
+      if (!pre_norm) {
+        gemm(cb, L.o, S, EPI_F32_RES, C_O, x32b, dp, y32b, dp, nullptr, res16 ? &xb : nullptr);
+        layernorm(y32b, S, L.g1, L.b1, res16 ? nullptr : x32b, &xb);
+        gemm(xb, L.w1, S, EPI_GELU_SPLIT, C_FFN1, nullptr, 0, nullptr, 0, &hb);
+        gemm(hb, L.w2, S, EPI_F32_RES, C_FFN2, x32b, dp, y32b, dp, nullptr, res16 ? &xb : nullptr);
+        layernorm(y32b, S, L.g2, L.b2, x32b, &xb);
+      } else {
+        gemm(cb, L.o, S, EPI_F32_RES, C_O, x32b, dp, y32b, dp, nullptr);
+        layernorm(y32b, S, L.g2, L.b2, nullptr, &xb);
+        gemm(xb, L.w1, S, EPI_GELU_SPLIT, C_FFN1, nullptr, 0, nullptr, 0, &hb);
+        gemm(hb, L.w2, S, EPI_F32_RES, C_FFN2, y32b, dp, x32b, dp, nullptr);
+      }
+    }
     {
       int e = ev_begin();
-      CK(launch_features(x32, dp, d, kind, d_cu, m, fa.hi, fa.lo, fa.ld, fmt, d_ovf, st));
+      CK(launch_features(layers.empty() ? x32 : x32b, dp, d, kind, layers.empty() ? d_cu : nullptr,
+                         m, fa.hi, fa.lo, fa.ld, fmt, d_ovf, st));
       ev_end(e, C_HEAD, 0, (double)m * (n_roles * d * 4 + F * (split ? 4 : 2)));
     }
     const Act* in = &fa;
