@@ -84,6 +84,11 @@ __device__ __forceinline__ void tmem_ld_32x16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void st_global_256(void* p, const uint32_t (&r)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
 __device__ __forceinline__ void tmem_st_1(uint32_t taddr, uint32_t v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
 }
@@ -158,7 +163,7 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
     }
     for (int s = 0; s < C::V_ST; ++s) {
       mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 8);  // released by the 8 warps of the item's group
+      mbar_init(&v_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
@@ -272,6 +277,7 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
           if (PSPLIT) tc_mma_ts(to, ph_ + 16, vh, idesc64, 1);
         }
         tc_commit(&o_full[b]);
+        tc_commit(&v_empty[s]);
       };
       int ks = 0, ko = 0;
       const long long t0 = clock64();
@@ -415,10 +421,7 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
       if (active) {
         const uint32_t to = tm + lane_off + 256 + b * 128 + hf * 32;
         const float inv = 1.0f / (red_sum[r] + red_sum[128 + r]);
-        // Stage ctx rows in this item's V stage (the O MMAs finished reading V)
-        // as [row][128 B] per plane, 16-byte chunks XOR-swizzled by row, then
-        // each warp of the pair writes 16 whole 128-byte rows per plane.
-        uint8_t* stg = sm + C::QK_ST * C::QK_BYTES + (k % C::V_ST) * C::V_BYTES;
+        const size_t ob = (size_t)(t0 + r - ks) * ldc + h * 64 + hf * 32;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           float v[16];
@@ -429,38 +432,17 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] += w[i];
           }
-          // ctx is a convex combination of range-checked V rows: no fp16 overflow
-          uint32_t hh[8], ll[8];
+          if (r < ke) {
+            // ctx is a convex combination of range-checked V rows: no fp16 overflow;
+            // 16 pieces = 32 bytes per plane -> one 256-bit store each
+            uint32_t hh[8], ll[8];
 #pragma unroll
-          for (int i = 0; i < 16; i += 2) split2(v[i] * inv, v[i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int chunk = hf * 4 + half * 2 + u;
-            const uint32_t off = r * 128 + ((chunk ^ (r & 7)) << 4);
-            *reinterpret_cast<uint4*>(stg + off) =
-                make_uint4(hh[4 * u], hh[4 * u + 1], hh[4 * u + 2], hh[4 * u + 3]);
-            if (SPLIT)
-              *reinterpret_cast<uint4*>(stg + ATQ_TILE + off) =
-                  make_uint4(ll[4 * u], ll[4 * u + 1], ll[4 * u + 2], ll[4 * u + 3]);
-          }
-        }
-        pair_sync();
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int row = q * 32 + hf * 16 + i * 4 + (lane >> 3), chunk = lane & 7;
-          if (row < ke) {
-            const uint32_t off = row * 128 + ((chunk ^ (row & 7)) << 4);
-            const size_t o = (size_t)(t0 + row - ks) * ldc + h * 64 + chunk * 8;
-            *reinterpret_cast<uint4*>(ch + o) = *reinterpret_cast<const uint4*>(stg + off);
-            if (SPLIT)
-              *reinterpret_cast<uint4*>(cl + o) = *reinterpret_cast<const uint4*>(stg + ATQ_TILE + off);
+            for (int i = 0; i < 16; i += 2) split2(v[i] * inv, v[i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
+            st_global_256(ch + ob + half * 16, hh);
+            if (SPLIT) st_global_256(cl + ob + half * 16, ll);
           }
         }
       }
-      // generic-proxy staging traffic before the stage's next TMA (async proxy) fill
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&v_empty[k % C::V_ST]);
       tc_fence_before();
       if (tr) ATT_TRACE(k, 5);
     }
