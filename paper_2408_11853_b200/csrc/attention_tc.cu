@@ -28,7 +28,10 @@
 //
 // Roles (576 threads, one CTA per SM, items round-robin):
 //   warp 0       TMA producer: Q|K ring (QK_ST stages) and V ring (V_ST stages)
-//   warp 1       MMA issuer:   event loop over S(ks) and O(ko)
+//   warp 1       S issuer:     S(k) once its Q/K tiles landed and TMEM region k%2 is free
+//   warp 18      O issuer:     P·V(k) once P(k) and V(k) are ready
+//   (two issuer threads with blocking, hardware-suspended waits: neither queue
+//   ever waits behind the other)
 //   warps 2-9    group 0 (items k even, TMEM region 0): softmax, then epilogue
 //   warps 10-17  group 1 (items k odd,  TMEM region 1)
 // Inside a group two warps share each TMEM lane quarter (= 32 tile rows): warp
@@ -49,7 +52,7 @@
 
 namespace mfg {
 
-constexpr int ATQ_THREADS = 576;
+constexpr int ATQ_THREADS = 608;
 constexpr int ATQ_TILE = 128 * 128;  // 128 rows x 64 cols of 16-bit values (128B swizzle)
 
 template <int MODE>
@@ -228,11 +231,8 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
+    // ------------------------------------------------------------ S issuer
     if (lane == 0) {
-      // Event loop: S(ks) as soon as its Q/K tiles landed and its TMEM region is
-      // free, O(ko) as soon as P(ko) and V(ko) are ready (P(k) also implies
-      // that the group finished reading O(k-2)).
       auto issue_s = [&](int k) {
         const int b = k & 1;
         const int n16 = (att_tile_rows(tiles[item_of(k) / heads]) + 15) & ~15;
@@ -255,6 +255,17 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
         tc_commit(&s_full[b]);
         tc_commit(&qk_empty[s]);
       };
+      for (int k = 0; k < mine; ++k) {
+        if (k >= 2) mbar_wait(&o_full[k & 1], ((k - 2) >> 1) & 1);  // region free
+        mbar_wait(&qk_full[k % C::QK_ST], (k / C::QK_ST) & 1);
+        tc_fence_after();
+        ATT_TRACE(k, 0);
+        issue_s(k);
+      }
+    }
+  } else if (warp == 18) {
+    // ------------------------------------------------------------ O issuer
+    if (lane == 0) {
       auto issue_o = [&](int k) {
         const int b = k & 1;
         const int n16 = (att_tile_rows(tiles[item_of(k) / heads]) + 15) & ~15;
@@ -279,32 +290,15 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
         tc_commit(&o_full[b]);
         tc_commit(&v_empty[s]);
       };
-      int ks = 0, ko = 0;
-      const long long t0 = clock64();
-      while (ko < mine) {
-        bool progress = false;
-        if (ks < mine && ks <= ko + 1 &&
-            (ks < 2 || mbar_test(&o_full[ks & 1], ((ks - 2) >> 1) & 1)) &&
-            mbar_test(&qk_full[ks % C::QK_ST], (ks / C::QK_ST) & 1)) {
-          tc_fence_after();
-          ATT_TRACE(ks, 0);
-          issue_s(ks++);
-          progress = true;
-        }
-        if (ko < ks && mbar_test(&p_full[ko & 1], (ko >> 1) & 1) &&
-            mbar_test(&v_full[ko % C::V_ST], (ko / C::V_ST) & 1)) {
-          tc_fence_after();
-          ATT_TRACE(ko, 1);
-          issue_o(ko++);
-          progress = true;
-        }
-        if (!progress) {
-          __nanosleep(20);
-          if (clock64() - t0 > (1ll << 36)) __trap();  // protocol bug: never hang the GPU
-        }
+      for (int k = 0; k < mine; ++k) {
+        mbar_wait(&p_full[k & 1], (k >> 1) & 1);
+        mbar_wait(&v_full[k % C::V_ST], (k / C::V_ST) & 1);
+        tc_fence_after();
+        ATT_TRACE(k, 1);
+        issue_o(k);
       }
     }
-  } else {
+  } else if (warp < 18) {
     // ------------------------------------------------------------ softmax + epilogue
     const int g = (warp - 2) >> 3;          // group = region = item parity
     const int hf = ((warp - 2) >> 2) & 1;   // which half of the key chunks
