@@ -55,13 +55,22 @@ namespace mfg {
 constexpr int ATQ_THREADS = 608;
 constexpr int ATQ_TILE = 128 * 128;  // 128 rows x 64 cols of 16-bit values (128B swizzle)
 
-template <int MODE>
+constexpr int ATQ_TTILE = 128 * 32;  // 128 rows x 16 cols (32B swizzle): head-dim tail 64..79
+
+// DH = head dim, 64 or 80 (XLM-R XL). DH 80 keeps the first 64 columns of every
+// Q/K/V tile in the 128B-swizzled layout and the last 16 in a 32B-swizzled
+// "tail" tile: S = QKᵀ gets a 5th k-step from the tail tiles and P·V a second
+// N=16 product.
+template <int MODE, int DH>
 struct AtqCfg {
   static constexpr bool SPLIT = MODE == 3;
-  static constexpr int QK_BYTES = (SPLIT ? 4 : 2) * ATQ_TILE;  // Qh Kh (Ql Kl)
-  static constexpr int V_BYTES = (SPLIT ? 2 : 1) * ATQ_TILE;   // Vh (Vl)
+  static constexpr bool TAIL = DH == 80;
+  static constexpr int NPL_QK = SPLIT ? 4 : 2;  // Qh Kh (Ql Kl)
+  static constexpr int NPL_V = SPLIT ? 2 : 1;   // Vh (Vl)
+  static constexpr int QK_BYTES = NPL_QK * (ATQ_TILE + (TAIL ? ATQ_TTILE : 0));
+  static constexpr int V_BYTES = NPL_V * (ATQ_TILE + (TAIL ? ATQ_TTILE : 0));
   static constexpr int QK_ST = SPLIT ? 2 : 3;
-  static constexpr int V_ST = SPLIT ? 2 : 5;
+  static constexpr int V_ST = SPLIT ? (TAIL ? 1 : 2) : (TAIL ? 3 : 5);
   static constexpr int RED_OFF = QK_ST * QK_BYTES + V_ST * V_BYTES;  // [group][max|sum][half][row]
   static constexpr int BAR_OFF = RED_OFF + 2 * 2 * 2 * 128 * 4;
   static constexpr int SMEM = 1024 + BAR_OFF + 256;
@@ -91,6 +100,16 @@ __device__ __forceinline__ void st_global_256(void* p, const uint32_t (&r)[8]) {
   asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]), "r"(r[1]),
                "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
+}
+__device__ __forceinline__ void tmem_ld_32x8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void tmem_st_1(uint32_t taddr, uint32_t v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
@@ -136,13 +155,17 @@ __device__ __forceinline__ int att_tile_rows(const AttTile& t) {
   return n;
 }
 
-template <int MODE>
+template <int MODE, int DH>
 __global__ void __launch_bounds__(ATQ_THREADS, 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap mh,
-                        const __grid_constant__ CUtensorMap ml, const AttTile* __restrict__ tiles,
-                        int n_items, int heads, int d, float scale,
-                        int fmt, uint16_t* __restrict__ ch, uint16_t* __restrict__ cl, int ldc) {
-  using C = AtqCfg<MODE>;
+                        const __grid_constant__ CUtensorMap ml,
+                        const __grid_constant__ CUtensorMap th,
+                        const __grid_constant__ CUtensorMap tl_,
+                        const AttTile* __restrict__ tiles, int n_items, int heads, int d,
+                        float scale, int fmt, uint16_t* __restrict__ ch,
+                        uint16_t* __restrict__ cl, int ldc) {
+  using C = AtqCfg<MODE, DH>;
+  constexpr bool TAIL = C::TAIL;
   constexpr bool SPLIT = MODE == 3;     // Q, K, V as hi/lo pairs
   constexpr bool PSPLIT = MODE >= 2;    // P as hi/lo pair
   extern __shared__ uint8_t smem_raw[];
@@ -192,15 +215,17 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
         const int it = item_of(k);
         const AttTile tl = tiles[it / heads];
         const int h = it % heads;
-        const int cq = h * 64, ck = d + h * 64, cv = 2 * d + h * 64;
+        const int cq = h * DH, ck = d + h * DH, cv = 2 * d + h * DH;
         int rows32 = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) rows32 += (tl.len[j] + 31) & ~31;
+        const int row_bytes = 128 + (TAIL ? 32 : 0);
         {
           const int s = k % C::QK_ST;
           mbar_wait(&qk_empty[s], ((k / C::QK_ST) & 1) ^ 1);
-          mbar_expect_tx(&qk_full[s], rows32 * 128 * (SPLIT ? 4 : 2));
+          mbar_expect_tx(&qk_full[s], rows32 * row_bytes * C::NPL_QK);
           uint8_t* t = sm + s * C::QK_BYTES;
+          uint8_t* tt = t + C::NPL_QK * ATQ_TILE;  // tail tiles (DH 80)
           int o = 0;
           for (int j = 0; j < 4; ++j) {
             for (int r0 = 0; r0 < tl.len[j]; r0 += 32, o += 32) {
@@ -211,20 +236,33 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
                 tma_load_2d(t + 2 * ATQ_TILE + o * 128, &ml, &qk_full[s], cq, tok);
                 tma_load_2d(t + 3 * ATQ_TILE + o * 128, &ml, &qk_full[s], ck, tok);
               }
+              if (TAIL) {
+                tma_load_2d(tt + o * 32, &th, &qk_full[s], cq + 64, tok);
+                tma_load_2d(tt + ATQ_TTILE + o * 32, &th, &qk_full[s], ck + 64, tok);
+                if (SPLIT) {
+                  tma_load_2d(tt + 2 * ATQ_TTILE + o * 32, &tl_, &qk_full[s], cq + 64, tok);
+                  tma_load_2d(tt + 3 * ATQ_TTILE + o * 32, &tl_, &qk_full[s], ck + 64, tok);
+                }
+              }
             }
           }
         }
         {
           const int s = k % C::V_ST;
           mbar_wait(&v_empty[s], ((k / C::V_ST) & 1) ^ 1);
-          mbar_expect_tx(&v_full[s], rows32 * 128 * (SPLIT ? 2 : 1));
+          mbar_expect_tx(&v_full[s], rows32 * row_bytes * C::NPL_V);
           uint8_t* t = sm + C::QK_ST * C::QK_BYTES + s * C::V_BYTES;
+          uint8_t* tt = t + C::NPL_V * ATQ_TILE;
           int o = 0;
           for (int j = 0; j < 4; ++j) {
             for (int r0 = 0; r0 < tl.len[j]; r0 += 32, o += 32) {
               const int tok = tl.t0[j] + r0;
               tma_load_2d(t + o * 128, &mh, &v_full[s], cv, tok);
               if (SPLIT) tma_load_2d(t + ATQ_TILE + o * 128, &ml, &v_full[s], cv, tok);
+              if (TAIL) {
+                tma_load_2d(tt + o * 32, &th, &v_full[s], cv + 64, tok);
+                if (SPLIT) tma_load_2d(tt + ATQ_TTILE + o * 32, &tl_, &v_full[s], cv + 64, tok);
+              }
             }
           }
         }
@@ -250,6 +288,17 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
           if (SPLIT) {
             tc_mma_bf16(ts, ql + adv, kh + adv, idesc, 1);
             tc_mma_bf16(ts, qh + adv, kl + adv, idesc, 1);
+          }
+        }
+        if (TAIL) {  // head dims 64..79: one more k-step from the 32B-swizzled tail tiles
+          uint8_t* tt = t + C::NPL_QK * ATQ_TILE;
+          const uint64_t qht = umma_desc_sw32(tt), kht = umma_desc_sw32(tt + ATQ_TTILE);
+          tc_mma_bf16(ts, qht, kht, idesc, 1);
+          if (SPLIT) {
+            const uint64_t qlt = umma_desc_sw32(tt + 2 * ATQ_TTILE),
+                           klt = umma_desc_sw32(tt + 3 * ATQ_TTILE);
+            tc_mma_bf16(ts, qlt, kht, idesc, 1);
+            tc_mma_bf16(ts, qht, klt, idesc, 1);
           }
         }
         tc_commit(&s_full[b]);
@@ -278,14 +327,32 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
         const uint32_t idesc128 = idesc_f16kind(128, 128, fmt) | (1u << 16);
         uint8_t* t = sm + C::QK_ST * C::QK_BYTES + s * C::V_BYTES;
         const uint32_t tp = tm + b * 128, to = tm + 256 + b * 128;
+        const uint32_t idesc16 = idesc_f16kind(128, 16, fmt) | (1u << 16);
+        uint8_t* tt = t + C::NPL_V * ATQ_TILE;
         for (int kk = 0; kk < n16; kk += 16) {
           const uint32_t ph_ = tp + 32 * (kk >> 5) + 8 * ((kk >> 4) & 1);
           const uint64_t vh = umma_desc_sw128(t + kk * 128);
-          if (SPLIT)
-            tc_mma_ts(to, ph_, umma_desc_sw128_mn(t + kk * 128, ATQ_TILE), idesc128, kk != 0);
-          else
+          if (TAIL) {
+            // DH 80: O[0,64) from the main V tiles, O[64,80) from the tail tiles;
+            // hi·hi + lo·hi + hi·lo each (the [Vh | Vl] merge would need 160 columns)
+            const uint64_t vht = umma_desc_sw32_mn(tt + kk * 32);
             tc_mma_ts(to, ph_, vh, idesc64, kk != 0);
-          if (PSPLIT) tc_mma_ts(to, ph_ + 16, vh, idesc64, 1);
+            tc_mma_ts(to + 64, ph_, vht, idesc16, kk != 0);
+            if (PSPLIT) {
+              tc_mma_ts(to, ph_ + 16, vh, idesc64, 1);
+              tc_mma_ts(to + 64, ph_ + 16, vht, idesc16, 1);
+            }
+            if (SPLIT) {
+              tc_mma_ts(to, ph_, umma_desc_sw128(t + ATQ_TILE + kk * 128), idesc64, 1);
+              tc_mma_ts(to + 64, ph_, umma_desc_sw32_mn(tt + ATQ_TTILE + kk * 32), idesc16, 1);
+            }
+          } else {
+            if (SPLIT)
+              tc_mma_ts(to, ph_, umma_desc_sw128_mn(t + kk * 128, ATQ_TILE), idesc128, kk != 0);
+            else
+              tc_mma_ts(to, ph_, vh, idesc64, kk != 0);
+            if (PSPLIT) tc_mma_ts(to, ph_ + 16, vh, idesc64, 1);
+          }
         }
         tc_commit(&o_full[b]);
         tc_commit(&v_empty[s]);
@@ -415,12 +482,12 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
       if (active) {
         const uint32_t to = tm + lane_off + 256 + b * 128 + hf * 32;
         const float inv = 1.0f / (red_sum[r] + red_sum[128 + r]);
-        const size_t ob = (size_t)(t0 + r - ks) * ldc + h * 64 + hf * 32;
+        const size_t ob = (size_t)(t0 + r - ks) * ldc + h * DH + hf * 32;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           float v[16];
           tmem_ld_32x16(to + half * 16, v);
-          if (SPLIT) {  // O = Ph·Vh + Pl·Vh (columns 0..63) + Ph·Vl (64..127)
+          if (SPLIT && !TAIL) {  // O = Ph·Vh + Pl·Vh (columns 0..63) + Ph·Vl (64..127)
             float w[16];
             tmem_ld_32x16(to + 64 + half * 16, w);
 #pragma unroll
@@ -434,6 +501,18 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
             for (int i = 0; i < 16; i += 2) split2(v[i] * inv, v[i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
             st_global_256(ch + ob + half * 16, hh);
             if (SPLIT) st_global_256(cl + ob + half * 16, ll);
+          }
+        }
+        if (TAIL) {  // head dims 64..79: columns 64 + 8hf .. +7
+          float v[8];
+          tmem_ld_32x8(tm + lane_off + 256 + b * 128 + 64 + hf * 8, v);
+          if (r < ke) {
+            uint32_t hh[4], ll[4];
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) split2(v[i] * inv, v[i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
+            const size_t ot = (size_t)(t0 + r - ks) * ldc + h * DH + 64 + hf * 8;
+            *reinterpret_cast<uint4*>(ch + ot) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
+            if (SPLIT) *reinterpret_cast<uint4*>(cl + ot) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
           }
         }
       }
@@ -480,31 +559,40 @@ void att_plan_tiles(const int32_t* cu, int nseq, bool tc_ok, std::vector<AttTile
   if (nslot) tiles.push_back(cur);
 }
 
-template <int MODE>
-static void att_launch_tc(const CUtensorMap* mh, const CUtensorMap* ml, const AttTile* tiles,
-                          int n_items, int heads, int d, float scale, int fmt,
-                          uint16_t* ch, uint16_t* cl, int ldc, int grid, cudaStream_t st) {
-  constexpr int SM = AtqCfg<MODE>::SMEM;
-  cudaFuncSetAttribute(attention_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
-  attention_tc_kernel<MODE><<<grid, ATQ_THREADS, SM, st>>>(*mh, *ml, tiles, n_items, heads, d,
-                                                           scale, fmt, ch, cl, ldc);
+template <int MODE, int DH>
+static void att_launch_tc(const CUtensorMap* mh, const CUtensorMap* ml, const CUtensorMap* th,
+                          const CUtensorMap* tl, const AttTile* tiles, int n_items, int heads,
+                          int d, float scale, int fmt, uint16_t* ch, uint16_t* cl, int ldc,
+                          int grid, cudaStream_t st) {
+  constexpr int SM = AtqCfg<MODE, DH>::SMEM;
+  auto kern = attention_tc_kernel<MODE, DH>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
+  kern<<<grid, ATQ_THREADS, SM, st>>>(*mh, *ml, *th, *tl, tiles, n_items, heads, d, scale, fmt,
+                                      ch, cl, ldc);
 }
 
-cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml, int mode,
-                                const AttTile* tiles, int n_tiles, int heads, int d,
-                                int fmt, uint16_t* ch, uint16_t* cl, int ldc, int* ovf,
-                                int num_sms, cudaStream_t st) {
+cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml,
+                                const CUtensorMap* th, const CUtensorMap* tl, int mode,
+                                const AttTile* tiles, int n_tiles, int heads, int d, int fmt,
+                                uint16_t* ch, uint16_t* cl, int ldc, int* ovf, int num_sms,
+                                cudaStream_t st) {
   (void)ovf;  // ctx is a convex combination of range-checked V rows
   if (n_tiles <= 0) return cudaSuccess;
+  const int dh = d / heads;
+  if (dh != 64 && dh != 80) return cudaErrorInvalidValue;
   const float scale = 1.0f / sqrtf((float)d / (float)heads);
   const int n_items = n_tiles * heads;
   const int grid = n_items < num_sms ? n_items : num_sms;
-  if (mode == 3)
-    att_launch_tc<3>(mh, ml, tiles, n_items, heads, d, scale, fmt, ch, cl, ldc, grid, st);
-  else if (mode == 2)
-    att_launch_tc<2>(mh, mh, tiles, n_items, heads, d, scale, fmt, ch, cl, ldc, grid, st);
-  else
-    att_launch_tc<1>(mh, mh, tiles, n_items, heads, d, scale, fmt, ch, cl, ldc, grid, st);
+  const CUtensorMap* mlo = mode == 3 ? ml : mh;
+  const CUtensorMap* tlo = mode == 3 ? tl : th;
+#define ATT_GO(M, D) \
+  att_launch_tc<M, D>(mh, mlo, th, tlo, tiles, n_items, heads, d, scale, fmt, ch, cl, ldc, grid, st)
+  if (dh == 64) {
+    if (mode == 3) ATT_GO(3, 64); else if (mode == 2) ATT_GO(2, 64); else ATT_GO(1, 64);
+  } else {
+    if (mode == 3) ATT_GO(3, 80); else if (mode == 2) ATT_GO(2, 80); else ATT_GO(1, 80);
+  }
+#undef ATT_GO
   return cudaGetLastError();
 }
 

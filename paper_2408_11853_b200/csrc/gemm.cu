@@ -30,6 +30,12 @@ static PFN_encodeTiled get_encode_fn() {
 
 bool make_tmap_u16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                     uint64_t ld_elems, uint32_t box_rows, char* err, size_t errcap) {
+  return make_tmap_u16_box(map, ptr, rows, cols, ld_elems, 64, box_rows, 128, err, errcap);
+}
+
+bool make_tmap_u16_box(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
+                       uint64_t ld_elems, uint32_t box_cols, uint32_t box_rows, int swizzle,
+                       char* err, size_t errcap) {
   PFN_encodeTiled enc = get_encode_fn();
   if (!enc) {
     snprintf(err, errcap, "cuTensorMapEncodeTiled unavailable from the driver");
@@ -37,10 +43,13 @@ bool make_tmap_u16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t co
   }
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {ld_elems * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapSwizzle sw = swizzle == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                : CU_TENSOR_MAP_SWIZZLE_32B;
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(ptr), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     snprintf(err, errcap, "cuTensorMapEncodeTiled failed (%d): rows=%llu cols=%llu ld=%llu box=%u",

@@ -21,7 +21,7 @@ cudaError_t launch_attention(const uint16_t* qh, const uint16_t* ql, int ldq, in
                              const int32_t* cu,
                              const int2* work, int n_work, uint16_t* ch, uint16_t* cl,
                              int ldc, int fmt, int* ovf, cudaStream_t st);
-// Persistent tcgen05 attention over (tile, head) items, d_head == 64. A tile
+// Persistent tcgen05 attention over (tile, head) items, d_head 64 or 80. A tile
 // holds up to 4 whole sequences of <= 128 tokens at 32-aligned tile rows
 // (att_plan_tiles). Maps: Q|K|V hi/lo [T][ldq] with box {64 cols, 32 rows}.
 // mode: 3 = Q/K/V and P as hi/lo pairs (3 MMAs per product), 2 = single Q/K/V,
@@ -30,7 +30,10 @@ struct AttTile {
   int t0[4];   // first token of each sequence (packed stream index)
   int len[4];  // its length (0 = unused slot)
 };
-cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml, int mode,
+// th/tl: the same Q|K|V planes with box {16 cols, 32 rows}, 32B swizzle (head
+// dims 64..79 of d_head 80; unused for d_head 64).
+cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml,
+                                const CUtensorMap* th, const CUtensorMap* tl, int mode,
                                 const AttTile* tiles, int n_tiles, int heads, int d, int fmt,
                                 uint16_t* ch, uint16_t* cl, int ldc, int* ovf, int num_sms,
                                 cudaStream_t st);
@@ -55,6 +58,10 @@ struct GemmArgs;
 // Encode a 2-D 16-bit K-major tensor map (128B swizzle, box = 64 x box_rows).
 bool make_tmap_u16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                     uint64_t ld_elems, uint32_t box_rows, char* err, size_t errcap);
+// General box: box_cols x box_rows, swizzle 128 / 64 / 32 bytes.
+bool make_tmap_u16_box(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
+                       uint64_t ld_elems, uint32_t box_cols, uint32_t box_rows, int swizzle,
+                       char* err, size_t errcap);
 // Largest supported N tile dividing n_pad (n_pad % 64 == 0).
 int gemm_pick_bn(int n_pad);
 // Whether N tile `bn` runs on the CTA-pair kernel, and the weight tensor-map box

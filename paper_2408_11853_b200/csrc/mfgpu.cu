@@ -101,6 +101,7 @@ struct mfg_ctx {
   bool att_tc = false;              // tcgen05 attention usable (d_head == 64)
   AttTile *d_tiles = nullptr, *h_tiles = nullptr;  // attention tiles (att_plan_tiles)
   CUtensorMap qm32h{}, qm32l{};     // Q|K|V maps with 32-row boxes (attention tiles)
+  CUtensorMap qt32h{}, qt32l{};     // ... 16-column tail boxes (d_head 80)
   std::vector<AttTile> v_tiles;
   std::vector<int2> v_work;
   std::vector<Act> ga;  // head hidden-stage outputs
@@ -347,8 +348,13 @@ struct mfg_ctx {
         throw Fail{MFG_ERR_RUNTIME, err};
       if (split && !make_tmap_u16(&qm32l, qa.lo, qa.rows, qa.ld, qa.ld, 32, err, sizeof err))
         throw Fail{MFG_ERR_RUNTIME, err};
+      if (!make_tmap_u16_box(&qt32h, qa.hi, qa.rows, qa.ld, qa.ld, 16, 32, 32, err, sizeof err))
+        throw Fail{MFG_ERR_RUNTIME, err};
+      if (split &&
+          !make_tmap_u16_box(&qt32l, qa.lo, qa.rows, qa.ld, qa.ld, 16, 32, 32, err, sizeof err))
+        throw Fail{MFG_ERR_RUNTIME, err};
     }
-    att_tc = (d / H == 64) && (d % 64 == 0);
+    att_tc = (d / H == 64 || d / H == 80) && (d % 64 == 0);
     make_act(xa, cap_tokens, dp);
     make_act(ca, cap_tokens, dp);
     make_act(ha, cap_tokens, fp);
@@ -455,8 +461,9 @@ struct mfg_ctx {
         const double bytes = (double)T * d * 4 * (split ? 4 : 2);
         int e = ev_begin();
         if (n_tiles > 0)
-          CK(launch_attention_tc(&qm32h, split ? &qm32l : &qm32h, split ? 3 : r16 ? 2 : 1, d_tiles,
-                                 n_tiles, H, d, fmt, ca.hi, ca.lo, ca.ld, d_ovf, num_sms, st));
+          CK(launch_attention_tc(&qm32h, split ? &qm32l : &qm32h, &qt32h, split ? &qt32l : &qt32h,
+                                 split ? 3 : r16 ? 2 : 1, d_tiles, n_tiles, H, d, fmt, ca.hi,
+                                 ca.lo, ca.ld, d_ovf, num_sms, st));
         if (n_work > 0)
           CK(launch_attention(qa.hi, qa.lo, qa.ld, d, H, d_cu, d_work, (int)n_work, ca.hi, ca.lo,
                               ca.ld, fmt, d_ovf, st));
@@ -933,7 +940,7 @@ extern "C" int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* c
     CK(cudaGetLastError());
     int32_t* dcu = s.alloc<int32_t>(n_seq + 1);
     CK(cudaMemcpy(dcu, cu, (n_seq + 1) * 4, cudaMemcpyHostToDevice));
-    const bool tc_ok = use_tc && (d / n_heads == 64) && (d % 64 == 0);
+    const bool tc_ok = use_tc && (d / n_heads == 64 || d / n_heads == 80) && (d % 64 == 0);
     std::vector<int2> work;
     std::vector<AttTile> tiles;
     att_plan_tiles(cu, n_seq, tc_ok, tiles, work);
@@ -946,15 +953,18 @@ extern "C" int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* c
     auto* ch = s.alloc<uint16_t>((size_t)T * ldc);
     auto* cl = split ? s.alloc<uint16_t>((size_t)T * ldc) : nullptr;
     if (!tiles.empty()) {
-      CUtensorMap mh, ml;
-      if (!make_tmap_u16(&mh, qh, Tp, ldq, ldq, 32, err, sizeof err))
+      CUtensorMap mh, ml, th, tl;
+      if (!make_tmap_u16(&mh, qh, Tp, ldq, ldq, 32, err, sizeof err) ||
+          !make_tmap_u16_box(&th, qh, Tp, ldq, ldq, 16, 32, 32, err, sizeof err))
         throw Fail{MFG_ERR_RUNTIME, err};
-      if (split && !make_tmap_u16(&ml, ql, Tp, ldq, ldq, 32, err, sizeof err))
+      if (split && (!make_tmap_u16(&ml, ql, Tp, ldq, ldq, 32, err, sizeof err) ||
+                    !make_tmap_u16_box(&tl, ql, Tp, ldq, ldq, 16, 32, 32, err, sizeof err)))
         throw Fail{MFG_ERR_RUNTIME, err};
       int sms = 148, dev = 0;
       CK(cudaGetDevice(&dev));
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      CK(launch_attention_tc(&mh, split ? &ml : &mh, split ? 3 : r16 ? 2 : 1, dt, (int)tiles.size(),
+      CK(launch_attention_tc(&mh, split ? &ml : &mh, &th, split ? &tl : &th, split ? 3 : r16 ? 2 : 1,
+                             dt, (int)tiles.size(),
                              n_heads, d, fmt, ch, cl, ldc, nullptr, sms, 0));
     }
     if (!work.empty())

@@ -231,6 +231,22 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_mn(const void* smem_tile, ui
   return d;
 }
 
+// 32-byte swizzle (16 16-bit values per row, 8-row / 256-byte atoms), K-major
+// operand or MN-major operand with a single 16-element atom in N.
+__device__ __forceinline__ uint64_t umma_desc_sw32(const void* smem_tile) {
+  const uint64_t addr = smem_u32(smem_tile);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;
+  d |= (uint64_t)1 << 16;              // LBO (unused)
+  d |= (uint64_t)(256 >> 4) << 32;     // SBO: 8 rows * 32 B
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;              // SWIZZLE_32B
+  return d;
+}
+__device__ __forceinline__ uint64_t umma_desc_sw32_mn(const void* smem_tile) {
+  return umma_desc_sw32(smem_tile);
+}
+
 // Instruction descriptor, kind::f16 -> fp32 accumulate, both operands K-major.
 // fmt: FMT_F16 (0) or FMT_BF16 (1) for both A and B.
 __host__ __device__ constexpr uint32_t idesc_f16kind(uint32_t M, uint32_t N, uint32_t fmt) {

@@ -102,7 +102,7 @@ def _attn_ref(qkv, cu, d, H):
                                       (1024, 16, [128, 3, 64, 100, 1, 33, 127, 129]),
                                       (256, 4, [512, 64, 65]), (2560, 32, [70, 9]),
                                       (1152, 18, [127, 5])])
-@pytest.mark.parametrize("prec", [0, 2, 1])
+@pytest.mark.parametrize("prec", [0, 2, 1, 3])
 @pytest.mark.parametrize("use_tc", [1, 0])
 def test_attention_parity(lib, d, H, lens, prec, use_tc):
     rng = np.random.default_rng(d + len(lens))
@@ -115,7 +115,7 @@ def test_attention_parity(lib, d, H, lens, prec, use_tc):
                             _p(qkv), _p(out), use_tc)
     assert rc == 0
     want = _attn_ref(qkv, cu, d, H)
-    tol = {0: 1e-5, 2: 1e-4, 1: 3e-2}[prec]
+    tol = {0: 1e-5, 2: 1e-4, 1: 3e-2, 3: 5e-3}[prec]
     assert np.abs(out - want).max() <= tol * (1 + np.abs(want).max())
 
 
