@@ -181,7 +181,11 @@ class Container {
     if (fstat(fd_, &st) != 0) throw std::runtime_error(path + ": stat failed");
     size_ = (size_t)st.st_size;
     if (size_ < 8 || size_ == 0) throw ContainerError(path + ": not a model container (bad magic)");
-    base_ = (const uint8_t*)mmap(nullptr, size_, PROT_READ, MAP_PRIVATE, fd_, 0);
+    // MAP_POPULATE: the weights are read once, front to back, right after open;
+    // pre-faulting the whole mapping in the kernel is much cheaper than taking
+    // one minor fault per 4 KB page from the upload threads.
+    base_ = (const uint8_t*)mmap(nullptr, size_, PROT_READ, MAP_PRIVATE | MAP_POPULATE, fd_, 0);
+    if (base_ != MAP_FAILED) madvise(const_cast<uint8_t*>(base_), size_, MADV_SEQUENTIAL);
     if (base_ == MAP_FAILED) {
       base_ = nullptr;
       throw std::runtime_error(path + ": mmap failed");

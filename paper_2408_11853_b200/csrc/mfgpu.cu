@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/mfgpu.h"
@@ -70,6 +71,66 @@ struct Layer {
 
 enum Cls { C_QKV = 0, C_O, C_FFN1, C_FFN2, C_ATT, C_LN, C_EMB, C_HEAD };
 
+// Host -> device weight upload (`container.py:363-412` mmap views -> HBM): the
+// mmap'd (page-cache) bytes are copied by several host threads into one of two
+// pinned chunks while the other chunk's async H2D copy (and the device-side
+// transpose/split of earlier matrices) runs, instead of a pageable cudaMemcpy
+// per tensor.
+struct Uploader {
+  static constexpr size_t CHUNK = 32u << 20;  // bytes per pinned chunk
+  cudaStream_t st = nullptr;
+  void* pinned[2] = {nullptr, nullptr};
+  cudaEvent_t free_ev[2] = {nullptr, nullptr};
+  bool used[2] = {false, false};
+  int cur = 0;
+  unsigned nthreads = 4;
+
+  void init(cudaStream_t s) {
+    st = s;
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaMallocHost(&pinned[i], CHUNK));
+      CK(cudaEventCreateWithFlags(&free_ev[i], cudaEventDisableTiming));
+    }
+    const unsigned hc = std::thread::hardware_concurrency();
+    nthreads = std::max(1u, std::min(8u, hc ? hc / 2 : 4u));
+  }
+  void release() {
+    for (int i = 0; i < 2; ++i) {
+      if (free_ev[i]) cudaEventSynchronize(free_ev[i]), cudaEventDestroy(free_ev[i]);
+      if (pinned[i]) cudaFreeHost(pinned[i]);
+      pinned[i] = nullptr;
+      free_ev[i] = nullptr;
+    }
+  }
+  ~Uploader() { release(); }
+  void par_copy(void* dst, const void* src, size_t n) {
+    if (n < (2u << 20) || nthreads <= 1) {
+      memcpy(dst, src, n);
+      return;
+    }
+    std::vector<std::thread> th;
+    const size_t part = (n + nthreads - 1) / nthreads;
+    for (unsigned i = 0; i < nthreads; ++i) {
+      const size_t a = i * part, b = std::min(n, a + part);
+      if (a >= b) break;
+      th.emplace_back([=] { memcpy((char*)dst + a, (const char*)src + a, b - a); });
+    }
+    for (auto& t : th) t.join();
+  }
+  // async: dst (device) <- src (host) bytes; src may be reused as soon as this returns
+  void upload(void* dst, const void* src, size_t n) {
+    for (size_t off = 0; off < n; off += CHUNK) {
+      const size_t k = std::min(CHUNK, n - off);
+      if (used[cur]) CK(cudaEventSynchronize(free_ev[cur]));
+      par_copy(pinned[cur], (const char*)src + off, k);
+      CK(cudaMemcpyAsync((char*)dst + off, pinned[cur], k, cudaMemcpyHostToDevice, st));
+      CK(cudaEventRecord(free_ev[cur], st));
+      used[cur] = true;
+      cur ^= 1;
+    }
+  }
+};
+
 }  // namespace
 
 struct mfg_ctx {
@@ -115,6 +176,9 @@ struct mfg_ctx {
   int64_t work_cap = 0;
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  Uploader* up = nullptr;  // weight upload pipeline (build() only)
+  size_t staging_half = 0;
+  int stage_flip = 0;
   std::vector<cudaEvent_t> pev;  // profile event pool
   struct Rec {
     int cls;
@@ -202,17 +266,18 @@ struct mfg_ctx {
     int row0 = 0;
     for (auto* m : mats) {
       const float* src = host_f32(*m, host_tmp);
-      CK(cudaMemcpyAsync(staging_dev, src, m->numel() * 4, cudaMemcpyHostToDevice, st));
-      CK(launch_transpose_split(staging_dev, (int)m->shape[0], (int)m->shape[1], w.hi, w.lo,
+      // two device staging halves alternate so the next matrix's H2D overlaps this transpose
+      float* stg = staging_dev + (stage_flip ^= 1) * staging_half;
+      up->upload(stg, src, m->numel() * 4);
+      CK(launch_transpose_split(stg, (int)m->shape[0], (int)m->shape[1], w.hi, w.lo,
                                 w.Kpad, row0, fmt, d_ovf, st));
-      CK(cudaStreamSynchronize(st));
       row0 += (int)m->shape[1];
     }
     w.bias = dalloc<float>(w.Npad);
     int off = 0;
     for (auto* b : biases) {
       const float* src = host_vec(*b, host_tmp);
-      CK(cudaMemcpy(w.bias + off, src, b->numel() * 4, cudaMemcpyHostToDevice));
+      up->upload(w.bias + off, src, b->numel() * 4);
       off += (int)b->numel();
     }
     if (!make_tmap_u16(&w.mh, w.hi, w.Npad, w.Kpad, w.Kpad, gemm_b_box_rows(w.bn), err, sizeof err))
@@ -256,12 +321,23 @@ struct mfg_ctx {
     std::vector<float> tmp;
     const float* src = host_vec(t, tmp);
     float* p = dalloc<float>(std::max<size_t>(pad_to, (size_t)t.numel()));
-    CK(cudaMemcpy(p, src, t.numel() * 4, cudaMemcpyHostToDevice));
+    up->upload(p, src, t.numel() * 4);
     return p;
   }
 
   void build(const mfg_config& cfg) {
+    // MFG_LOAD_TRACE=1: phase timings of the weight upload on stderr
+    const bool trace = getenv("MFG_LOAD_TRACE") != nullptr;
+    auto clk = [] { return std::chrono::steady_clock::now(); };
+    auto t_start = clk();
+    auto lap = [&](const char* what) {
+      if (!trace) return;
+      cudaStreamSynchronize(st);
+      fprintf(stderr, "mfg load: %-12s %8.1f ms\n", what,
+              std::chrono::duration<double, std::milli>(clk() - t_start).count());
+    };
     Container c(cfg.container_path);
+    lap("open");
     man = c.manifest();
     if (man.like == "comet-qe") { kind = 0; n_roles = 2; }
     else if (man.like == "comet") { kind = 1; n_roles = 3; }
@@ -296,12 +372,18 @@ struct mfg_ctx {
         big = std::max(big, n);
       }
     float* staging = nullptr;
-    CK(cudaMalloc(&staging, std::max<int64_t>(big, 1) * 4));
+    staging_half = (size_t)std::max<int64_t>(big, 1);
+    CK(cudaMalloc(&staging, staging_half * 2 * 4));
+    Uploader uploader;
+    uploader.init(st);
+    up = &uploader;
     std::vector<float> tmp;
     d_ovf = dalloc<int>(1);
     CK(cudaMallocHost(&h_ovf, sizeof(int)));
     try {
+      lap("setup");
       tok = upload_vec(*c.find("emb.tok"));
+      lap("emb.tok");
       pos = upload_vec(*c.find("emb.pos"));
       layers.resize(man.n_layers);
       for (int i = 0; i < man.n_layers; ++i) {
@@ -318,6 +400,7 @@ struct mfg_ctx {
         L.g2 = upload_vec(*T(".norm2.g"));
         L.b2 = upload_vec(*T(".norm2.b"));
       }
+      lap("layers");
       const size_t stages = man.head_hidden.size() + 1;
       head.resize(stages);
       for (size_t j = 0; j < stages; ++j) {
@@ -325,10 +408,13 @@ struct mfg_ctx {
         make_weight(head[j], {c.find(p + ".w")}, {c.find(p + ".b")}, staging, tmp);
       }
     } catch (...) {
+      cudaStreamSynchronize(st);
+      up = nullptr;
       cudaFree(staging);
       throw;
     }
     CK(cudaStreamSynchronize(st));
+    up = nullptr;
     CK(cudaFree(staging));
     CK(cudaMemcpy(h_ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost));
     if (*h_ovf)
@@ -336,6 +422,7 @@ struct mfg_ctx {
                                 "(|w| >= 65520); use precision bf16x3"};
     qkv_ld = layers.empty() ? pad64(3 * d) : layers[0].qkv.Npad;
 
+    lap("weights");
     // workspaces
     cap_tokens = pad128(cfg.max_tokens > 0 ? cfg.max_tokens : 262144);
     cap_records = cfg.max_records > 0 ? cfg.max_records : 4096;
