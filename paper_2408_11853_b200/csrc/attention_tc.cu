@@ -541,8 +541,8 @@ void att_plan_tiles(const int32_t* cu, int nseq, bool tc_ok, std::vector<AttTile
   int used = 0, nslot = 0;  // 32-row granules used, sequences in `cur`
   for (int s = 0; s < nseq; ++s) {
     const int a = cu[s], L = cu[s + 1] - a;
-    if (!tc_ok || L > 128) {
-      for (int q = 0; q < L; q += 64) work.push_back(make_int2(s, q));
+    if (!tc_ok || L > 128) {  // SIMT: 64-query blocks; tcgen05 long kernel: 128-query blocks
+      for (int q = 0; q < L; q += tc_ok ? 128 : 64) work.push_back(make_int2(s, q));
       continue;
     }
     const int R = (L + 31) & ~31;

@@ -37,9 +37,16 @@ cudaError_t launch_attention_tc(const CUtensorMap* mh, const CUtensorMap* ml,
                                 const AttTile* tiles, int n_tiles, int heads, int d, int fmt,
                                 uint16_t* ch, uint16_t* cl, int ldc, int* ovf, int num_sms,
                                 cudaStream_t st);
+// tcgen05 attention for sequences of 129..512 tokens: one CTA per (work item,
+// head), two passes over 128-key blocks (row stats, then P·V). Same maps/modes.
+cudaError_t launch_attention_long(const CUtensorMap* mh, const CUtensorMap* ml,
+                                  const CUtensorMap* th, const CUtensorMap* tl, int mode,
+                                  const int2* work, int n_work, const int32_t* cu, int heads, int d,
+                                  int fmt, uint16_t* ch, uint16_t* cl, int ldc, cudaStream_t st);
 cudaError_t att_set_trace(long long* dev_buf);  // diagnostics: [4][64][8] clock64 or null
-// Host: sequences of <= 128 tokens (when tc_ok) -> tiles; the rest -> SIMT
-// work items {seq, q0} (64-query blocks).
+// Host: sequences of <= 128 tokens (when tc_ok) -> tiles; longer ones -> work
+// items {seq, q0} for launch_attention_long (128-query blocks); without tc_ok
+// every sequence -> SIMT work items (64-query blocks).
 void att_plan_tiles(const int32_t* cu, int nseq, bool tc_ok, std::vector<AttTile>& tiles,
                     std::vector<int2>& work);
 cudaError_t launch_features(const float* x, int ld, int d, int kind, const int32_t* cu, int n,

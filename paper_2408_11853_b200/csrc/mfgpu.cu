@@ -551,7 +551,11 @@ struct mfg_ctx {
           CK(launch_attention_tc(&qm32h, split ? &qm32l : &qm32h, &qt32h, split ? &qt32l : &qt32h,
                                  split ? 3 : r16 ? 2 : 1, d_tiles, n_tiles, H, d, fmt, ca.hi,
                                  ca.lo, ca.ld, d_ovf, num_sms, st));
-        if (n_work > 0)
+        if (n_work > 0 && att_tc)
+          CK(launch_attention_long(&qm32h, split ? &qm32l : &qm32h, &qt32h,
+                                   split ? &qt32l : &qt32h, split ? 3 : r16 ? 2 : 1, d_work,
+                                   (int)n_work, d_cu, H, d, fmt, ca.hi, ca.lo, ca.ld, st));
+        else if (n_work > 0)
           CK(launch_attention(qa.hi, qa.lo, qa.ld, d, H, d_cu, d_work, (int)n_work, ca.hi, ca.lo,
                               ca.ld, fmt, d_ovf, st));
         ev_end(e, C_ATT, 4.0 * sum_l2 * d, bytes);
@@ -1039,22 +1043,27 @@ extern "C" int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* c
       CK(cudaMemcpy(dt, tiles.data(), tiles.size() * sizeof(AttTile), cudaMemcpyHostToDevice));
     auto* ch = s.alloc<uint16_t>((size_t)T * ldc);
     auto* cl = split ? s.alloc<uint16_t>((size_t)T * ldc) : nullptr;
-    if (!tiles.empty()) {
-      CUtensorMap mh, ml, th, tl;
+    CUtensorMap mh, ml, th, tl;
+    if (tc_ok) {
       if (!make_tmap_u16(&mh, qh, Tp, ldq, ldq, 32, err, sizeof err) ||
           !make_tmap_u16_box(&th, qh, Tp, ldq, ldq, 16, 32, 32, err, sizeof err))
         throw Fail{MFG_ERR_RUNTIME, err};
       if (split && (!make_tmap_u16(&ml, ql, Tp, ldq, ldq, 32, err, sizeof err) ||
                     !make_tmap_u16_box(&tl, ql, Tp, ldq, ldq, 16, 32, 32, err, sizeof err)))
         throw Fail{MFG_ERR_RUNTIME, err};
+    }
+    const int mode = split ? 3 : r16 ? 2 : 1;
+    if (!tiles.empty()) {
       int sms = 148, dev = 0;
       CK(cudaGetDevice(&dev));
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      CK(launch_attention_tc(&mh, split ? &ml : &mh, &th, split ? &tl : &th, split ? 3 : r16 ? 2 : 1,
-                             dt, (int)tiles.size(),
-                             n_heads, d, fmt, ch, cl, ldc, nullptr, sms, 0));
+      CK(launch_attention_tc(&mh, split ? &ml : &mh, &th, split ? &tl : &th, mode, dt,
+                             (int)tiles.size(), n_heads, d, fmt, ch, cl, ldc, nullptr, sms, 0));
     }
-    if (!work.empty())
+    if (!work.empty() && tc_ok)
+      CK(launch_attention_long(&mh, split ? &ml : &mh, &th, split ? &tl : &th, mode, dw,
+                               (int)work.size(), dcu, n_heads, d, fmt, ch, cl, ldc, 0));
+    else if (!work.empty())
       CK(launch_attention(qh, ql, ldq, d, n_heads, dcu, dw, (int)work.size(), ch, cl, ldc, fmt,
                           nullptr, 0));
     float* o = s.alloc<float>((size_t)T * d);

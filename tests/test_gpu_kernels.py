@@ -101,6 +101,7 @@ def _attn_ref(qkv, cu, d, H):
 @pytest.mark.parametrize("d,H,lens", [(16, 2, [3, 1, 7]), (64, 1, [65, 2, 130, 16, 17]),
                                       (1024, 16, [128, 3, 64, 100, 1, 33, 127, 129]),
                                       (256, 4, [512, 64, 65]), (2560, 32, [70, 9]),
+                                      (2560, 32, [300, 9, 129]), (320, 4, [511, 200]),
                                       (1152, 18, [127, 5])])
 @pytest.mark.parametrize("prec", [0, 2, 1, 3])
 @pytest.mark.parametrize("use_tc", [1, 0])
