@@ -108,6 +108,7 @@ __device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, in
                                          int n0, int half, float* buf, int lane) {
   const int cg = lane & 7;       // transposed phase: 4 columns 4*cg..4*cg+3
   const int rs = lane >> 3;      // row sub-index 0..3
+  if (rows <= 0) return;         // warp-uniform: this quarter of the tile is past M
 #pragma unroll 1
   for (int c = half * 32; c < BN; c += 32 * NSUB) {
     const int col = n0 + c + 4 * cg;

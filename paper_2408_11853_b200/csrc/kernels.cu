@@ -299,6 +299,59 @@ __global__ void __launch_bounds__(ATT_THREADS)
   }
 }
 
+// ------------------------------------------------------------------ BOS-query attention
+// Last layer: pooling reads only row 0 of each sequence (`encoder.py:181-185`), so
+// only the BOS query of every (sequence, head) is needed. One warp per (s, h):
+// scores over all keys of the sequence in fp32 from the hi(+lo) pieces, the
+// reference's max / exp / sum (`masked_softmax`, `encoder.py:60-66`), ctx = Σ p v / sum.
+// q: compact [S][ldqb] (this sequence's Q row), K|V: packed Q|K|V rows of qa.
+__global__ void __launch_bounds__(32)
+    bos_attention_kernel(const uint16_t* __restrict__ qbh, const uint16_t* __restrict__ qbl,
+                         int ldqb, const uint16_t* __restrict__ kvh,
+                         const uint16_t* __restrict__ kvl, int ldkv, int d, int dh, float scale,
+                         const int32_t* __restrict__ cu, uint16_t* __restrict__ ch,
+                         uint16_t* __restrict__ cl, int ldc, int fmt) {
+  __shared__ float qs[128];
+  __shared__ float ps[512];
+  const int s = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
+  const int start = cu[s], L = cu[s + 1] - start;
+  for (int c = lane; c < dh; c += 32) {
+    const size_t o = (size_t)s * ldqb + h * dh + c;
+    qs[c] = load16(qbh, o, fmt) + (qbl ? load16(qbl, o, fmt) : 0.f);
+  }
+  __syncwarp();
+  float mx = -INFINITY;
+  for (int j = lane; j < L; j += 32) {
+    const size_t ko = (size_t)(start + j) * ldkv + d + h * dh;
+    float acc = 0.f;
+    for (int c = 0; c < dh; ++c) {
+      const float k = load16(kvh, ko + c, fmt) + (kvl ? load16(kvl, ko + c, fmt) : 0.f);
+      acc = fmaf(qs[c], k, acc);
+    }
+    ps[j] = acc * scale;
+    mx = fmaxf(mx, acc * scale);
+  }
+  mx = warp_max(mx);
+  __syncwarp();
+  float sum = 0.f;
+  for (int j = lane; j < L; j += 32) {
+    const float p = expf(ps[j] - mx);
+    ps[j] = p;
+    sum += p;
+  }
+  sum = warp_sum(sum);
+  __syncwarp();
+  const float inv = 1.0f / sum;
+  for (int c = lane; c < dh; c += 32) {
+    float acc = 0.f;
+    for (int j = 0; j < L; ++j) {
+      const size_t vo = (size_t)(start + j) * ldkv + 2 * d + h * dh + c;
+      acc = fmaf(ps[j], load16(kvh, vo, fmt) + (kvl ? load16(kvl, vo, fmt) : 0.f), acc);
+    }
+    store_split(ch, cl, (size_t)s * ldc + h * dh + c, acc * inv, fmt, nullptr);
+  }
+}
+
 // ------------------------------------------------------------------ features
 // BOS pooling (`encoder.py:181-185`) + per-kind feature vector (`:198-212`),
 // written as the bf16 hi/lo A-operand of the first head GEMM.
@@ -439,6 +492,19 @@ cudaError_t launch_attention(const uint16_t* qh, const uint16_t* ql, int ldq, in
   ATT_CASE(1) ATT_CASE(2) ATT_CASE(4) ATT_CASE(8) ATT_CASE(10) ATT_CASE(12) ATT_CASE(16)
 #undef ATT_CASE
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_bos_attention(const uint16_t* qbh, const uint16_t* qbl, int ldqb,
+                                 const uint16_t* kvh, const uint16_t* kvl, int ldkv, int d,
+                                 int heads, const int32_t* cu, int nseq, uint16_t* ch, uint16_t* cl,
+                                 int ldc, int fmt, cudaStream_t st) {
+  if (nseq <= 0) return cudaSuccess;
+  const int dh = d / heads;
+  if (dh > 128) return cudaErrorInvalidValue;
+  const float scale = 1.0f / sqrtf((float)d / (float)heads);
+  bos_attention_kernel<<<dim3(nseq, heads), 32, 0, st>>>(qbh, qbl, ldqb, kvh, kvl, ldkv, d, dh,
+                                                         scale, cu, ch, cl, ldc, fmt);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_features(const float* x, int ld, int d, int kind, const int32_t* cu, int n,

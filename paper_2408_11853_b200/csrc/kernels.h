@@ -49,6 +49,13 @@ cudaError_t att_set_trace(long long* dev_buf);  // diagnostics: [4][64][8] clock
 // every sequence -> SIMT work items (64-query blocks).
 void att_plan_tiles(const int32_t* cu, int nseq, bool tc_ok, std::vector<AttTile>& tiles,
                     std::vector<int2>& work);
+// Attention for the BOS query of every sequence only (last layer): q compact
+// [nseq][ldqb], K|V from the packed Q|K|V rows [T][ldkv]; ctx -> compact [nseq][ldc].
+// Sequences of <= 512 tokens, d_head <= 128.
+cudaError_t launch_bos_attention(const uint16_t* qbh, const uint16_t* qbl, int ldqb,
+                                 const uint16_t* kvh, const uint16_t* kvl, int ldkv, int d,
+                                 int heads, const int32_t* cu, int nseq, uint16_t* ch, uint16_t* cl,
+                                 int ldc, int fmt, cudaStream_t st);
 cudaError_t launch_features(const float* x, int ld, int d, int kind, const int32_t* cu, int n,
                             uint16_t* fh, uint16_t* fl, int ldf, int fmt, int* ovf,
                             cudaStream_t st);

@@ -66,6 +66,7 @@ struct Act {
 
 struct Layer {
   Weight qkv, o, w1, w2;
+  Weight q_part, kv_part;  // views of qkv: rows [0,d) and [d,3d) (last layer only)
   float *g1 = nullptr, *b1 = nullptr, *g2 = nullptr, *b2 = nullptr;
 };
 
@@ -156,8 +157,9 @@ struct mfg_ctx {
   int cap_records = 0;
   float *x32 = nullptr, *y32 = nullptr;
   Act xa, ca, ha, fa, qa;          // qa: Q|K|V pieces [T][qkv_ld]
-  // last layer on BOS rows only (one row per sequence): ctx, residual/LN, FFN hidden
-  Act cb, xb, hb;
+  // last layer on BOS rows only (one row per sequence): ctx, residual/LN, FFN hidden, Q
+  Act cb, xb, hb, qb;
+  bool bos_qkv = false;  // last layer: K|V for all rows, Q + attention for BOS rows only
   float *x32b = nullptr, *y32b = nullptr;
   bool att_tc = false;              // tcgen05 attention usable (d_head == 64)
   AttTile *d_tiles = nullptr, *h_tiles = nullptr;  // attention tiles (att_plan_tiles)
@@ -401,6 +403,34 @@ struct mfg_ctx {
         L.b2 = upload_vec(*T(".norm2.b"));
       }
       lap("layers");
+      // last layer's Q / K|V views of the fused QKV weight (needs d % 64 == 0 so the
+      // split falls on a padded-row boundary, and tile-aligned N for both parts)
+      if (!layers.empty() && d % 64 == 0) {
+        Weight& w = layers.back().qkv;
+        const int bq = gemm_pick_bn(d), bkv = gemm_pick_bn(2 * d);
+        bos_qkv = w.N == 3 * d;
+        auto view = [&](Weight& v, int row0, int n, int bn) {
+          char err[256];
+          v = Weight{};
+          v.hi = w.hi + (size_t)row0 * w.Kpad;
+          v.lo = w.lo ? w.lo + (size_t)row0 * w.Kpad : nullptr;
+          v.bias = w.bias + row0;
+          v.N = n;
+          v.K = w.K;
+          v.Npad = n;
+          v.Kpad = w.Kpad;
+          v.bn = bn;
+          if (!make_tmap_u16(&v.mh, v.hi, n, v.Kpad, v.Kpad, gemm_b_box_rows(bn), err, sizeof err))
+            throw Fail{MFG_ERR_RUNTIME, err};
+          if (v.lo && !make_tmap_u16(&v.ml, v.lo, n, v.Kpad, v.Kpad, gemm_b_box_rows(bn), err,
+                                     sizeof err))
+            throw Fail{MFG_ERR_RUNTIME, err};
+        };
+        if (bos_qkv) {
+          view(layers.back().q_part, 0, d, bq);
+          view(layers.back().kv_part, d, 2 * d, bkv);
+        }
+      }
       const size_t stages = man.head_hidden.size() + 1;
       head.resize(stages);
       for (size_t j = 0; j < stages; ++j) {
@@ -451,6 +481,7 @@ struct mfg_ctx {
       make_act(cb, ns, dp);
       make_act(xb, ns, dp);
       make_act(hb, ns, fp);
+      make_act(qb, ns, dp);
       x32b = dalloc<float>((size_t)pad128(ns) * dp);
       y32b = dalloc<float>((size_t)pad128(ns) * dp);
     }
@@ -475,7 +506,7 @@ struct mfg_ctx {
 
   // ---------------------------------------------------------------- forward
   void gemm(const Act& a, const Weight& w, int M, int epi, int cls, const float* res, int ldr,
-            float* out32, int ldo, Act* outa, const Act* res16 = nullptr) {
+            float* out32, int ldo, Act* outa, const Act* res16 = nullptr, int out_col = 0) {
     GemmArgs g{};
     g.M = M;
     g.N = w.Npad;
@@ -494,8 +525,8 @@ struct mfg_ctx {
     g.ovf = d_ovf;
     g.r16 = r16;
     if (outa) {
-      g.out_hi = outa->hi;
-      g.out_lo = outa->lo;
+      g.out_hi = outa->hi + out_col;
+      g.out_lo = outa->lo ? outa->lo + out_col : nullptr;
       g.ldh = outa->ld;
     }
     int e = ev_begin();
@@ -517,7 +548,8 @@ struct mfg_ctx {
   // One device chunk: m records, T tokens, role-major packing in h_* staging.
   // One device chunk: m records, T tokens; ids already in d_ids (role-major),
   // cu / work items in the pinned h_* staging. Scores land in dscores[0..m).
-  void forward_chunk(int m, int64_t T, int64_t n_work, int n_tiles, double sum_l2) {
+  void forward_chunk(int m, int64_t T, int64_t n_work, int n_tiles, double sum_l2, int max_l) {
+    const bool bos_q = bos_qkv && max_l <= 512;  // BOS attention kernel keeps <= 512 scores
     const int nseq = m * n_roles;
     CK(cudaMemcpyAsync(d_cu, h_cu, (nseq + 1) * 4, cudaMemcpyHostToDevice, st));
     if (n_tiles > 0)
@@ -539,10 +571,30 @@ struct mfg_ctx {
       ev_end(e, C_EMB, 0, (double)T * d * (8 + (res16 ? 0 : 4) + (pre_norm ? 0 : (split ? 4 : 2))));
     }
     const bool res16 = !pre_norm && (split || r16) && !layers.empty();
+    const int S = nseq;
+    // BOS rows of xa (the layer input pieces) and, when the residual is fp32, of x32
+    auto gather_inputs = [&]() {
+      int e = ev_begin();
+      CK(launch_gather_bos(d_cu, S, d, xa.hi, xa.lo, xa.ld, res16 ? nullptr : x32, dp, xb.hi,
+                           xb.lo, xb.ld, x32b, dp, st));
+      ev_end(e, C_HEAD, 0, (double)S * d * 12);
+    };
     for (size_t li = 0; li < layers.size(); ++li) {
       Layer& L = layers[li];
       const bool last = li + 1 == layers.size();
       if (pre_norm) layernorm(x32, Ti, L.g1, L.b1, nullptr, &xa);
+      if (last && bos_q) {
+        // Last layer: only BOS queries are pooled, so Q (and attention) run on one
+        // row per sequence; K and V still cover every token.
+        gather_inputs();
+        gemm(xa, L.kv_part, Ti, EPI_SPLIT, C_QKV, nullptr, 0, nullptr, 0, &qa, nullptr, d);
+        gemm(xb, L.q_part, S, EPI_SPLIT, C_QKV, nullptr, 0, nullptr, 0, &qb);
+        int e = ev_begin();
+        CK(launch_bos_attention(qb.hi, qb.lo, qb.ld, qa.hi, qa.lo, qa.ld, d, H, d_cu, S, cb.hi,
+                                cb.lo, cb.ld, fmt, st));
+        ev_end(e, C_ATT, 4.0 * (double)T * d, (double)T * 2 * d * (split ? 4 : 2));
+        break;
+      }
       gemm(xa, L.qkv, Ti, EPI_SPLIT, C_QKV, nullptr, 0, nullptr, 0, &qa);
       {
         const double bytes = (double)T * d * 4 * (split ? 4 : 2);
@@ -580,17 +632,12 @@ struct mfg_ctx {
     // LayerNorms and the FFN run on one row per sequence (bitwise the same values).
     if (!layers.empty()) {
       Layer& L = layers.back();
-      const int S = nseq;
-      {
+      if (!bos_q) {  // full last-layer attention: gather its BOS rows
         int e = ev_begin();
-        const bool res_pieces = res16;
         CK(launch_gather_bos(d_cu, S, d, ca.hi, ca.lo, ca.ld, nullptr, 0, cb.hi, cb.lo, cb.ld,
                              nullptr, 0, st));
-        CK(launch_gather_bos(d_cu, S, d, res_pieces ? xa.hi : nullptr,
-                             res_pieces ? xa.lo : nullptr, xa.ld, res_pieces ? nullptr : x32, dp,
-                             xb.hi, xb.lo, xb.ld, x32b, dp, st));
-        stats.kernel_launches += 1;
-        ev_end(e, C_HEAD, 0, (double)S * d * 16);
+        ev_end(e, C_HEAD, 0, (double)S * d * 8);
+        gather_inputs();
       }
       if (!pre_norm) {
         gemm(cb, L.o, S, EPI_F32_RES, C_O, x32b, dp, y32b, dp, nullptr, res16 ? &xb : nullptr);
@@ -688,6 +735,7 @@ struct mfg_ctx {
       // role-major chunk: cu / work items on the host, ids staged per role
       int64_t at = 0;
       double sum_l2 = 0;
+      int64_t max_l = 0;
       h_cu[0] = 0;
       for (int k = 0; k < n_roles; ++k) {
         const int64_t s0 = (int64_t)k * n + r0, s1 = (int64_t)k * n + r1;
@@ -701,6 +749,7 @@ struct mfg_ctx {
           const int ls = (int)(k * m + (s - s0));
           h_cu[ls + 1] = (int32_t)(at + (cu[s + 1] - cu[s0]));
           sum_l2 += (double)L * L;
+          max_l = std::max<int64_t>(max_l, L);
         }
         at += len;
       }
@@ -708,7 +757,7 @@ struct mfg_ctx {
       std::copy(v_tiles.begin(), v_tiles.end(), h_tiles);
       std::copy(v_work.begin(), v_work.end(), h_work);
       if (!device_io) CK(cudaMemcpyAsync(d_ids, h_ids, T * 4, cudaMemcpyHostToDevice, st));
-      forward_chunk(m, T, (int64_t)v_work.size(), (int)v_tiles.size(), sum_l2);
+      forward_chunk(m, T, (int64_t)v_work.size(), (int)v_tiles.size(), sum_l2, (int)max_l);
       if (device_io) {
         CK(cudaMemcpyAsync(out + r0, dscores, m * 4, cudaMemcpyDeviceToDevice, st));
         check_flag();
