@@ -41,8 +41,9 @@ struct GemmArgs {
   int ldr;
   const uint16_t* res_hi;    // ... or, when non-null, 16-bit hi (+ lo) pieces [M][ldr]
   const uint16_t* res_lo;    //     in `fmt` (residual stream kept as operand pieces)
-  float* out_f32;            // [M][ldo] (EPI_F32*)
+  float* out_f32;            // [M][ldo] (EPI_F32*) ...
   int ldo;
+  uint16_t* out16;           // ... or, when non-null, binary16 [M][ldo] (reference fp16 mode)
   uint16_t* out_hi;          // [M][ldh] (split epilogues), 16-bit pieces in `fmt`
   uint16_t* out_lo;          // may be null when the consumer GEMM is not split
   int ldh;
@@ -169,8 +170,15 @@ __device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, in
               x[0] = round16(x[0]); x[1] = round16(x[1]); x[2] = round16(x[2]); x[3] = round16(x[3]);
             }
           }
-          *reinterpret_cast<float4*>(args.out_f32 + o * args.ldo + col) =
-              make_float4(x[0], x[1], x[2], x[3]);
+          if (args.out16) {
+            const __half2 a = __floats2half2_rn(x[0], x[1]), b2 = __floats2half2_rn(x[2], x[3]);
+            *reinterpret_cast<uint2*>(args.out16 + o * args.ldo + col) =
+                make_uint2(*reinterpret_cast<const uint32_t*>(&a),
+                           *reinterpret_cast<const uint32_t*>(&b2));
+          } else {
+            *reinterpret_cast<float4*>(args.out_f32 + o * args.ldo + col) =
+                make_float4(x[0], x[1], x[2], x[3]);
+          }
         } else {
           float y[4];
 #pragma unroll

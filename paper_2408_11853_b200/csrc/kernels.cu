@@ -41,59 +41,82 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __r
 // out = (y - mean) / sqrt(var_pop + 1e-5) * g + b, one warp per row
 // (`encoder.py:52-57, 128-130`). Writes any of: fp32 copy, 16-bit hi, lo pieces.
 // V4 float4 per lane (d % 4 == 0), two-pass statistics from registers.
-template <int V4>
+// IN16: the input row holds binary16 values (reference fp16 mode: the residual
+// sum is already rounded to fp16), 2 instead of 4 bytes per element.
+// One warp per row (a persistent row loop and a prefetched next row were both
+// measured slower: fewer rows in flight per SM).
+template <int V4, bool IN16>
+__device__ __forceinline__ void ln_load_row(const void* __restrict__ yv, int t, int ld, int n4,
+                                            int lane, float4 (&v)[V4]) {
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    const int c = i * 32 + lane;
+    if (c >= n4) {
+      v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else if (IN16) {
+      const uint2 u = reinterpret_cast<const uint2*>(
+          reinterpret_cast<const uint16_t*>(yv) + (size_t)t * ld)[c];
+      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+      v[i] = make_float4(a.x, a.y, b.x, b.y);
+    } else {
+      v[i] = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(yv) +
+                                             (size_t)t * ld)[c];
+    }
+  }
+}
+
+template <int V4, bool IN16>
 __global__ void __launch_bounds__(256)
-    layernorm_kernel(const float* __restrict__ y, int T, int d, int ld,
+    layernorm_kernel(const void* __restrict__ yv, int T, int d, int ld,
                      const float* __restrict__ g, const float* __restrict__ bta,
                      float* __restrict__ out32, uint16_t* __restrict__ oh,
                      uint16_t* __restrict__ ol, int fmt, int r16, int* ovf) {
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (t >= T) return;
-  const float4* row = reinterpret_cast<const float4*>(y + (size_t)t * ld);
   const int n4 = d >> 2;
-  float4 v[V4];
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < V4; ++i) {
-    const int c = i * 32 + lane;
-    v[i] = c < n4 ? row[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-  }
-  const float mean = warp_sum(s) / (float)d;
-  float q = 0.f;
-#pragma unroll
-  for (int i = 0; i < V4; ++i) {
-    if (i * 32 + lane < n4) {
-      const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, e = v[i].w - mean;
-      q += (a * a + b * b) + (c * c + e * e);
-    }
-  }
-  const float rstd = 1.0f / sqrtf(warp_sum(q) / (float)d + 1e-5f);
-  const size_t o = (size_t)t * ld;
   bool ok = true;
+  {
+    const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (t >= T) return;
+    float4 v[V4];
+    ln_load_row<V4, IN16>(yv, t, ld, n4, lane, v);
+    float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < V4; ++i) {
-    const int c = i * 32 + lane;
-    if (c < n4) {
-      const float4 gg = reinterpret_cast<const float4*>(g)[c];
-      const float4 bb = reinterpret_cast<const float4*>(bta)[c];
-      float r[4] = {(v[i].x - mean) * rstd * gg.x + bb.x, (v[i].y - mean) * rstd * gg.y + bb.y,
-                    (v[i].z - mean) * rstd * gg.z + bb.z, (v[i].w - mean) * rstd * gg.w + bb.w};
-      if (r16) {
+    for (int i = 0; i < V4; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    const float mean = warp_sum(s) / (float)d;
+    float q = 0.f;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) r[j] = __half2float(__float2half_rn(r[j]));
+    for (int i = 0; i < V4; ++i) {
+      if (i * 32 + lane < n4) {
+        const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, e = v[i].w - mean;
+        q += (a * a + b * b) + (c * c + e * e);
       }
-      if (out32) reinterpret_cast<float4*>(out32 + o)[c] = make_float4(r[0], r[1], r[2], r[3]);
-      if (oh) {
-        uint16_t h[4], l[4];
+    }
+    const float rstd = 1.0f / sqrtf(warp_sum(q) / (float)d + 1e-5f);
+    const size_t o = (size_t)t * ld;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ok &= split16(r[j], fmt, h[j], l[j]);
-        reinterpret_cast<uint2*>(oh + o)[c] =
-            make_uint2(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16));
-        if (ol)
-          reinterpret_cast<uint2*>(ol + o)[c] =
-              make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
+    for (int i = 0; i < V4; ++i) {
+      const int c = i * 32 + lane;
+      if (c < n4) {
+        const float4 gg = reinterpret_cast<const float4*>(g)[c];
+        const float4 bb = reinterpret_cast<const float4*>(bta)[c];
+        float r[4] = {(v[i].x - mean) * rstd * gg.x + bb.x, (v[i].y - mean) * rstd * gg.y + bb.y,
+                      (v[i].z - mean) * rstd * gg.z + bb.z, (v[i].w - mean) * rstd * gg.w + bb.w};
+        if (r16) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) r[j] = __half2float(__float2half_rn(r[j]));
+        }
+        if (out32) reinterpret_cast<float4*>(out32 + o)[c] = make_float4(r[0], r[1], r[2], r[3]);
+        if (oh) {
+          // fp16 range: |r| >= 65520 rounds to inf -> flag (one test per 4 values)
+          if (fmt == FMT_F16)
+            ok &= !(fmaxf(fmaxf(fabsf(r[0]), fabsf(r[1])), fmaxf(fabsf(r[2]), fabsf(r[3]))) >= 65520.f);
+          uint32_t h01, h23, l01, l23;
+          split2(r[0], r[1], fmt, h01, l01);
+          split2(r[2], r[3], fmt, h23, l23);
+          reinterpret_cast<uint2*>(oh + o)[c] = make_uint2(h01, h23);
+          if (ol) reinterpret_cast<uint2*>(ol + o)[c] = make_uint2(l01, l23);
+        }
       }
     }
   }
@@ -101,23 +124,30 @@ __global__ void __launch_bounds__(256)
 }
 
 // Scalar fallback for d % 4 != 0.
-__global__ void layernorm_scalar_kernel(const float* __restrict__ y, int T, int d, int ld,
-                                        const float* __restrict__ g, const float* __restrict__ bta,
+__device__ __forceinline__ float ln_in(const void* y, int in16, size_t i) {
+  return in16 ? __half2float(__ushort_as_half(reinterpret_cast<const uint16_t*>(y)[i]))
+              : reinterpret_cast<const float*>(y)[i];
+}
+__global__ void layernorm_scalar_kernel(const void* __restrict__ y, int in16, int T, int d,
+                                        int ld, const float* __restrict__ g,
+                                        const float* __restrict__ bta,
                                         float* __restrict__ out32, uint16_t* __restrict__ oh,
                                         uint16_t* __restrict__ ol, int fmt, int r16, int* ovf) {
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
-  const float* row = y + (size_t)t * ld;
+  const size_t o = (size_t)t * ld;
   float s = 0.f;
-  for (int c = lane; c < d; c += 32) s += row[c];
+  for (int c = lane; c < d; c += 32) s += ln_in(y, in16, o + c);
   const float mean = warp_sum(s) / (float)d;
   float q = 0.f;
-  for (int c = lane; c < d; c += 32) q += (row[c] - mean) * (row[c] - mean);
-  const float rstd = 1.0f / sqrtf(warp_sum(q) / (float)d + 1e-5f);
-  const size_t o = (size_t)t * ld;
   for (int c = lane; c < d; c += 32) {
-    float r = (row[c] - mean) * rstd * g[c] + bta[c];
+    const float a = ln_in(y, in16, o + c) - mean;
+    q += a * a;
+  }
+  const float rstd = 1.0f / sqrtf(warp_sum(q) / (float)d + 1e-5f);
+  for (int c = lane; c < d; c += 32) {
+    float r = (ln_in(y, in16, o + c) - mean) * rstd * g[c] + bta[c];
     if (r16) r = __half2float(__float2half_rn(r));
     if (out32) out32[o + c] = r;
     if (oh) store_split(oh, ol, o + c, r, fmt, ovf);
@@ -442,25 +472,40 @@ cudaError_t launch_embed(const int32_t* ids, const int32_t* cu, int nseq, int V,
   return cudaGetLastError();
 }
 
-cudaError_t launch_layernorm(const float* y, int T, int d, int ld, const float* g, const float* b,
+template <int V4, bool IN16>
+static cudaError_t ln_launch(const void* y, int T, int d, int ld, const float* g, const float* b,
                              float* out32, uint16_t* oh, uint16_t* ol, int fmt, int r16, int* ovf,
-                             cudaStream_t st) {
+                             int rows_blocks, cudaStream_t st) {
+  // 4 rows (warps) per CTA: small CTAs retire as soon as their rows are done
+  layernorm_kernel<V4, IN16><<<(T + 3) / 4, 128, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol, fmt,
+                                                          r16, ovf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_layernorm(const void* y, int in16, int T, int d, int ld, const float* g,
+                             const float* b, float* out32, uint16_t* oh, uint16_t* ol, int fmt,
+                             int r16, int* ovf, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  dim3 grid((T + 7) / 8), block(256);
+  const int rows_blocks = (T + 7) / 8;
+  dim3 block(256);
   const bool vec = d % 4 == 0 && ld % 4 == 0 && ((uintptr_t)y & 15) == 0 &&
                    ((uintptr_t)g & 15) == 0 && ((uintptr_t)b & 15) == 0;
   const int v4 = (d / 4 + 31) / 32;
   if (vec) {
 #define LN_CASE(V)                                                                   \
     if (v4 <= V) {                                                                   \
-      layernorm_kernel<V><<<grid, block, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol, fmt, r16, ovf); \
-      return cudaGetLastError();                                                     \
+      if (in16)                                                                      \
+        return ln_launch<V, true>(y, T, d, ld, g, b, out32, oh, ol, fmt, r16, ovf,       \
+                                  rows_blocks, st);                                  \
+      return ln_launch<V, false>(y, T, d, ld, g, b, out32, oh, ol, fmt, r16, ovf,        \
+                                 rows_blocks, st);                                   \
     }
     LN_CASE(1) LN_CASE(2) LN_CASE(4) LN_CASE(8) LN_CASE(9) LN_CASE(10) LN_CASE(12) LN_CASE(16)
     LN_CASE(20) LN_CASE(24) LN_CASE(32)
 #undef LN_CASE
   }
-  layernorm_scalar_kernel<<<grid, block, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol, fmt, r16, ovf);
+  layernorm_scalar_kernel<<<rows_blocks, block, 0, st>>>(y, in16, T, d, ld, g, b, out32, oh, ol,
+                                                         fmt, r16, ovf);
   return cudaGetLastError();
 }
 

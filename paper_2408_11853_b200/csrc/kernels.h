@@ -12,9 +12,10 @@ namespace mfg {
 cudaError_t launch_embed(const int32_t* ids, const int32_t* cu, int nseq, int V, int d,
                          const float* tok, const float* pe, float* x32, int ld, uint16_t* xh,
                          uint16_t* xl, int fmt, int r16, int* flag, cudaStream_t st);
-cudaError_t launch_layernorm(const float* y, int T, int d, int ld, const float* g, const float* b,
-                             float* out32, uint16_t* oh, uint16_t* ol, int fmt, int r16, int* ovf,
-                             cudaStream_t st);
+// y: fp32 rows, or binary16 rows when in16 (reference fp16 mode residual sums).
+cudaError_t launch_layernorm(const void* y, int in16, int T, int d, int ld, const float* g,
+                             const float* b, float* out32, uint16_t* oh, uint16_t* ol, int fmt,
+                             int r16, int* ovf, cudaStream_t st);
 // SIMT fp32 attention over (sequence, 64-query block) work items; Q|K|V read as
 // hi(+lo) 16-bit pieces [T][ldq].
 cudaError_t launch_attention(const uint16_t* qh, const uint16_t* ql, int ldq, int d, int heads,

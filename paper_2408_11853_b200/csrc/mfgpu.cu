@@ -506,7 +506,8 @@ struct mfg_ctx {
 
   // ---------------------------------------------------------------- forward
   void gemm(const Act& a, const Weight& w, int M, int epi, int cls, const float* res, int ldr,
-            float* out32, int ldo, Act* outa, const Act* res16 = nullptr, int out_col = 0) {
+            float* out32, int ldo, Act* outa, const Act* res16 = nullptr, int out_col = 0,
+            bool as16 = false) {
     GemmArgs g{};
     g.M = M;
     g.N = w.Npad;
@@ -519,7 +520,8 @@ struct mfg_ctx {
       g.res_lo = res16->lo;
       g.ldr = res16->ld;
     }
-    g.out_f32 = out32;
+    g.out_f32 = as16 ? nullptr : out32;
+    g.out16 = as16 ? reinterpret_cast<uint16_t*>(out32) : nullptr;
     g.ldo = ldo;
     g.fmt = fmt;
     g.ovf = d_ovf;
@@ -538,11 +540,13 @@ struct mfg_ctx {
     ev_end(e, cls, flops, bytes);
   }
 
-  void layernorm(const float* y, int T, const float* g, const float* b, float* out32, Act* a) {
+  void layernorm(const float* y, int T, const float* g, const float* b, float* out32, Act* a,
+                 bool in16 = false) {
     int e = ev_begin();
-    CK(launch_layernorm(y, T, d, dp, g, b, out32, a ? a->hi : nullptr, a ? a->lo : nullptr, fmt,
-                        r16, d_ovf, st));
-    ev_end(e, C_LN, 0, (double)T * d * (4 + (out32 ? 4 : 0) + (a ? (split ? 4 : 2) : 0)));
+    CK(launch_layernorm(y, in16, T, d, dp, g, b, out32, a ? a->hi : nullptr,
+                        a ? a->lo : nullptr, fmt, r16, d_ovf, st));
+    ev_end(e, C_LN, 0,
+           (double)T * d * ((in16 ? 2 : 4) + (out32 ? 4 : 0) + (a ? (split ? 4 : 2) : 0)));
   }
 
   // One device chunk: m records, T tokens, role-major packing in h_* staging.
@@ -571,6 +575,7 @@ struct mfg_ctx {
       ev_end(e, C_EMB, 0, (double)T * d * (8 + (res16 ? 0 : 4) + (pre_norm ? 0 : (split ? 4 : 2))));
     }
     const bool res16 = !pre_norm && (split || r16) && !layers.empty();
+    const bool y16 = res16 && r16;  // O-proj / FFN2 outputs as binary16 (reference fp16 mode)
     const int S = nseq;
     // BOS rows of xa (the layer input pieces) and, when the residual is fp32, of x32
     auto gather_inputs = [&]() {
@@ -615,11 +620,14 @@ struct mfg_ctx {
       }
       if (last) break;  // the last layer's O-proj / FFN run on the BOS rows only (below)
       if (!pre_norm) {
-        gemm(ca, L.o, Ti, EPI_F32_RES, C_O, x32, dp, y32, dp, nullptr, res16 ? &xa : nullptr);
-        layernorm(y32, Ti, L.g1, L.b1, res16 ? nullptr : x32, &xa);
+        // reference fp16 mode: the rounded residual sums travel as binary16
+        gemm(ca, L.o, Ti, EPI_F32_RES, C_O, x32, dp, y32, dp, nullptr, res16 ? &xa : nullptr, 0,
+             y16);
+        layernorm(y32, Ti, L.g1, L.b1, res16 ? nullptr : x32, &xa, y16);
         gemm(xa, L.w1, Ti, EPI_GELU_SPLIT, C_FFN1, nullptr, 0, nullptr, 0, &ha);
-        gemm(ha, L.w2, Ti, EPI_F32_RES, C_FFN2, x32, dp, y32, dp, nullptr, res16 ? &xa : nullptr);
-        layernorm(y32, Ti, L.g2, L.b2, res16 ? nullptr : x32, &xa);
+        gemm(ha, L.w2, Ti, EPI_F32_RES, C_FFN2, x32, dp, y32, dp, nullptr, res16 ? &xa : nullptr, 0,
+             y16);
+        layernorm(y32, Ti, L.g2, L.b2, res16 ? nullptr : x32, &xa, y16);
       } else {
         gemm(ca, L.o, Ti, EPI_F32_RES, C_O, x32, dp, y32, dp, nullptr);
         layernorm(y32, Ti, L.g2, L.b2, nullptr, &xa);
@@ -640,11 +648,13 @@ struct mfg_ctx {
         gather_inputs();
       }
       if (!pre_norm) {
-        gemm(cb, L.o, S, EPI_F32_RES, C_O, x32b, dp, y32b, dp, nullptr, res16 ? &xb : nullptr);
-        layernorm(y32b, S, L.g1, L.b1, res16 ? nullptr : x32b, &xb);
+        gemm(cb, L.o, S, EPI_F32_RES, C_O, x32b, dp, y32b, dp, nullptr, res16 ? &xb : nullptr, 0,
+             y16);
+        layernorm(y32b, S, L.g1, L.b1, res16 ? nullptr : x32b, &xb, y16);
         gemm(xb, L.w1, S, EPI_GELU_SPLIT, C_FFN1, nullptr, 0, nullptr, 0, &hb);
-        gemm(hb, L.w2, S, EPI_F32_RES, C_FFN2, x32b, dp, y32b, dp, nullptr, res16 ? &xb : nullptr);
-        layernorm(y32b, S, L.g2, L.b2, x32b, &xb);
+        gemm(hb, L.w2, S, EPI_F32_RES, C_FFN2, x32b, dp, y32b, dp, nullptr, res16 ? &xb : nullptr, 0,
+             y16);
+        layernorm(y32b, S, L.g2, L.b2, x32b, &xb, y16);
       } else {
         gemm(cb, L.o, S, EPI_F32_RES, C_O, x32b, dp, y32b, dp, nullptr);
         layernorm(y32b, S, L.g2, L.b2, nullptr, &xb);
@@ -1152,7 +1162,7 @@ extern "C" int mfgt_layernorm(int32_t T, int32_t d, const float* y, const float*
     CK(cudaMemcpy(dy, y, (size_t)T * d * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dg, g, d * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(db, b, d * 4, cudaMemcpyHostToDevice));
-    CK(launch_layernorm(dy, T, d, d, dg, db, dout, nullptr, nullptr, FMT_BF16, 0, nullptr, 0));
+    CK(launch_layernorm(dy, 0, T, d, d, dg, db, dout, nullptr, nullptr, FMT_BF16, 0, nullptr, 0));
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out, dout, (size_t)T * d * 4, cudaMemcpyDeviceToHost));
   });
