@@ -335,50 +335,83 @@ __global__ void __launch_bounds__(ATT_THREADS)
 // scores over all keys of the sequence in fp32 from the hi(+lo) pieces, the
 // reference's max / exp / sum (`masked_softmax`, `encoder.py:60-66`), ctx = Σ p v / sum.
 // q: compact [S][ldqb] (this sequence's Q row), K|V: packed Q|K|V rows of qa.
-__global__ void __launch_bounds__(32)
+// 16-bit pieces -> fp32 for 8 consecutive values (one 16-byte load per plane)
+__device__ __forceinline__ void load8(const uint16_t* __restrict__ hi, const uint16_t* __restrict__ lo,
+                                      size_t o, int fmt, float (&v)[8]) {
+  const uint4 h = *reinterpret_cast<const uint4*>(hi + o);
+  const uint16_t* hp = reinterpret_cast<const uint16_t*>(&h);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = load16(hp, i, fmt);
+  if (lo) {
+    const uint4 l = *reinterpret_cast<const uint4*>(lo + o);
+    const uint16_t* lp = reinterpret_cast<const uint16_t*>(&l);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] += load16(lp, i, fmt);
+  }
+}
+
+// 4 warps per CTA, warp w -> head 4*blockIdx.y + w of sequence blockIdx.x.
+// Requires dh % 8 == 0 and 16-byte aligned rows (true for the padded layouts).
+__global__ void __launch_bounds__(128)
     bos_attention_kernel(const uint16_t* __restrict__ qbh, const uint16_t* __restrict__ qbl,
                          int ldqb, const uint16_t* __restrict__ kvh,
-                         const uint16_t* __restrict__ kvl, int ldkv, int d, int dh, float scale,
-                         const int32_t* __restrict__ cu, uint16_t* __restrict__ ch,
+                         const uint16_t* __restrict__ kvl, int ldkv, int d, int dh, int heads,
+                         float scale, const int32_t* __restrict__ cu, uint16_t* __restrict__ ch,
                          uint16_t* __restrict__ cl, int ldc, int fmt) {
-  __shared__ float qs[128];
-  __shared__ float ps[512];
-  const int s = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
+  __shared__ float qs[4][128];
+  __shared__ float ps[4][512];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x, h = blockIdx.y * 4 + w;
+  if (h >= heads) return;
   const int start = cu[s], L = cu[s + 1] - start;
   for (int c = lane; c < dh; c += 32) {
     const size_t o = (size_t)s * ldqb + h * dh + c;
-    qs[c] = load16(qbh, o, fmt) + (qbl ? load16(qbl, o, fmt) : 0.f);
+    qs[w][c] = load16(qbh, o, fmt) + (qbl ? load16(qbl, o, fmt) : 0.f);
   }
   __syncwarp();
   float mx = -INFINITY;
   for (int j = lane; j < L; j += 32) {
     const size_t ko = (size_t)(start + j) * ldkv + d + h * dh;
     float acc = 0.f;
-    for (int c = 0; c < dh; ++c) {
-      const float k = load16(kvh, ko + c, fmt) + (kvl ? load16(kvl, ko + c, fmt) : 0.f);
-      acc = fmaf(qs[c], k, acc);
+    for (int c = 0; c < dh; c += 8) {
+      float k[8];
+      load8(kvh, kvl, ko + c, fmt, k);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc = fmaf(qs[w][c + i], k[i], acc);
     }
-    ps[j] = acc * scale;
+    ps[w][j] = acc * scale;
     mx = fmaxf(mx, acc * scale);
   }
   mx = warp_max(mx);
   __syncwarp();
   float sum = 0.f;
   for (int j = lane; j < L; j += 32) {
-    const float p = expf(ps[j] - mx);
-    ps[j] = p;
+    const float p = expf(ps[w][j] - mx);
+    ps[w][j] = p;
     sum += p;
   }
   sum = warp_sum(sum);
   __syncwarp();
   const float inv = 1.0f / sum;
   for (int c = lane; c < dh; c += 32) {
-    float acc = 0.f;
-    for (int j = 0; j < L; ++j) {
-      const size_t vo = (size_t)(start + j) * ldkv + 2 * d + h * dh + c;
-      acc = fmaf(ps[j], load16(kvh, vo, fmt) + (kvl ? load16(kvl, vo, fmt) : 0.f), acc);
+    // 4 keys per step with independent partial sums: the V loads of a step are
+    // in flight together (one dependent chain per warp was latency-bound)
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const size_t vo = (size_t)start * ldkv + 2 * d + h * dh + c;
+    int j = 0;
+    for (; j + 4 <= L; j += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const size_t o = vo + (size_t)(j + u) * ldkv;
+        acc[u] = fmaf(ps[w][j + u], load16(kvh, o, fmt) + (kvl ? load16(kvl, o, fmt) : 0.f), acc[u]);
+      }
     }
-    store_split(ch, cl, (size_t)s * ldc + h * dh + c, acc * inv, fmt, nullptr);
+    for (; j < L; ++j) {
+      const size_t o = vo + (size_t)j * ldkv;
+      acc[0] = fmaf(ps[w][j], load16(kvh, o, fmt) + (kvl ? load16(kvl, o, fmt) : 0.f), acc[0]);
+    }
+    const float total = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    store_split(ch, cl, (size_t)s * ldc + h * dh + c, total * inv, fmt, nullptr);
   }
 }
 
@@ -547,8 +580,9 @@ cudaError_t launch_bos_attention(const uint16_t* qbh, const uint16_t* qbl, int l
   const int dh = d / heads;
   if (dh > 128) return cudaErrorInvalidValue;
   const float scale = 1.0f / sqrtf((float)d / (float)heads);
-  bos_attention_kernel<<<dim3(nseq, heads), 32, 0, st>>>(qbh, qbl, ldqb, kvh, kvl, ldkv, d, dh,
-                                                         scale, cu, ch, cl, ldc, fmt);
+  if (dh % 8) return cudaErrorInvalidValue;
+  bos_attention_kernel<<<dim3(nseq, (heads + 3) / 4), 128, 0, st>>>(
+      qbh, qbl, ldqb, kvh, kvl, ldkv, d, dh, heads, scale, cu, ch, cl, ldc, fmt);
   return cudaGetLastError();
 }
 

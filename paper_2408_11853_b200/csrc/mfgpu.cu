@@ -408,7 +408,7 @@ struct mfg_ctx {
       if (!layers.empty() && d % 64 == 0) {
         Weight& w = layers.back().qkv;
         const int bq = gemm_pick_bn(d), bkv = gemm_pick_bn(2 * d);
-        bos_qkv = w.N == 3 * d;
+        bos_qkv = w.N == 3 * d && (d / H) % 8 == 0;
         auto view = [&](Weight& v, int row0, int n, int bn) {
           char err[256];
           v = Weight{};
