@@ -23,6 +23,13 @@ int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, int32_t K, c
 int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* cu, int32_t d,
                    int32_t n_heads, const float* qkv, float* ctx_out, int32_t use_tc);
 
+/* Host-only (no device needed): the attention work planner. Sequences of <= 128
+ * tokens go into tiles of <= 4 whole sequences at 32-aligned rows (tiles_out: per
+ * tile t0[4] then len[4]); longer ones into {seq, q0} items of 128 queries
+ * (64 when tc_ok == 0: every sequence goes to the SIMT kernel). */
+int mfgt_plan_tiles(const int32_t* cu, int32_t nseq, int32_t tc_ok, int32_t* tiles_out,
+                    int32_t* n_tiles, int32_t* work_out, int32_t* n_work, int32_t cap);
+
 /* Diagnostics: enable = 1 starts recording a clock64 trace of the tcgen05
  * attention kernel (first 4 CTAs x 64 items x 8 events); enable = 0 stops and
  * copies it to host_out[2048]. */

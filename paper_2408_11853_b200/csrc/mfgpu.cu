@@ -1133,6 +1133,29 @@ extern "C" int mfgt_attention(int32_t precision, int32_t n_seq, const int32_t* c
   });
 }
 
+// Host-only: the attention work planner (att_plan_tiles) for CPU tests.
+// tiles_out: n_tiles x {t0[4], len[4]}; work_out: n_work x {seq, q0}.
+extern "C" int mfgt_plan_tiles(const int32_t* cu, int32_t nseq, int32_t tc_ok, int32_t* tiles_out,
+                               int32_t* n_tiles, int32_t* work_out, int32_t* n_work,
+                               int32_t cap) {
+  std::vector<AttTile> tiles;
+  std::vector<int2> work;
+  att_plan_tiles(cu, nseq, tc_ok != 0, tiles, work);
+  if ((int64_t)tiles.size() > cap || (int64_t)work.size() > cap) return MFG_ERR_USAGE;
+  for (size_t i = 0; i < tiles.size(); ++i)
+    for (int j = 0; j < 4; ++j) {
+      tiles_out[i * 8 + j] = tiles[i].t0[j];
+      tiles_out[i * 8 + 4 + j] = tiles[i].len[j];
+    }
+  for (size_t i = 0; i < work.size(); ++i) {
+    work_out[2 * i] = work[i].x;
+    work_out[2 * i + 1] = work[i].y;
+  }
+  *n_tiles = (int32_t)tiles.size();
+  *n_work = (int32_t)work.size();
+  return MFG_OK;
+}
+
 // Diagnostics: route the next attention launches' per-item clock64 trace to a
 // device buffer (enable = 1), or copy it to host_out[4*64*8] and stop (enable = 0).
 extern "C" int mfgt_att_trace(int32_t enable, long long* host_out) {

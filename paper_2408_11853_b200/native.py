@@ -118,6 +118,8 @@ def gpu():
             lib.mfgt_layernorm.restype = C.c_int
             lib.mfgt_att_trace.argtypes = [i32, C.POINTER(C.c_longlong)]
             lib.mfgt_att_trace.restype = C.c_int
+            lib.mfgt_plan_tiles.argtypes = [i32p, i32, i32, i32p, i32p, i32p, i32p, i32]
+            lib.mfgt_plan_tiles.restype = C.c_int
             _gpu = lib
     return _gpu
 
