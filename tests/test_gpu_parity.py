@@ -241,3 +241,43 @@ def test_fp16_mode_midsize_vs_oracle_fp16(golden, fixture_dir):
         got = ev.evaluate_lines(lines).segment_scores
     d = np.abs(np.array(got) - np.array(want))
     assert d.max() <= 2e-3, d.max()
+
+
+def test_empty_and_degenerate_inputs(tiny_comet):
+    """No records -> empty report (system None); empty fields ([BOS EOS] only),
+    a single record and one record per window all score like the oracle."""
+    with make_ev(tiny_comet) as ev:
+        rep = ev.evaluate_lines([])
+        assert rep.segment_scores == [] and rep.system_score is None
+    lines = ["\t\t", "a\t\t", "\tb\t", "the cat\t\tthe"]
+    want, _ = oe.score_lines(OracleModel(tiny_comet.manifest, tiny_comet.weights),
+                             otk.OracleVocab(fx.fixture_vocab_lines()), lines)
+    with make_ev(tiny_comet) as ev:
+        got = ev.evaluate_lines(lines).segment_scores
+        one = [ev.evaluate_lines([ln]).segment_scores[0] for ln in lines]
+    assert np.abs(np.array(got) - np.array(want)).max() <= 5e-5
+    assert got == one  # bitwise: a record's score does not depend on its window
+
+
+def test_long_and_short_sequences_at_xlmr_width(golden, fixture_dir):
+    """d 1024 / 16 heads with sequences of 2..400 tokens in one window: packed
+    128-row tiles, the two-pass long-sequence kernel, the BOS-only last layer and
+    max_len truncation all against the oracle (fp32 parity path)."""
+    man = dict(golden["midsize"]["manifest"], max_position=512)
+    w = dict(fx.synthetic_weights(man))
+    path = write_model(fixture_dir / "mid_long.mfrg", man, w)
+    vlines = fx.synthetic_vocab_lines(man["vocab_size"])
+    vpath = fx.write_vocab(fixture_dir / "mid_long_vocab.txt", vlines)
+    rng = np.random.default_rng(5)
+    n_words = man["vocab_size"] - len(fx.SPECIALS)
+
+    def text(n):
+        return " ".join(f"w{i}" for i in rng.integers(0, n_words, n))
+
+    sizes = [0, 1, 30, 126, 127, 128, 200, 300, 398, 600]
+    lines = ["\t".join(text(int(rng.choice(sizes))) for _ in range(3)) for _ in range(12)]
+    want, _ = oe.score_lines(OracleModel(man, w), otk.OracleVocab(vlines), lines, max_len=512)
+    with mf.Evaluator(mf.EvaluatorConfig(model=path, vocab=vpath, quiet=True)) as ev:
+        got = ev.evaluate_lines(lines).segment_scores
+    d = np.abs(np.array(got) - np.array(want))
+    assert d.max() <= 5e-5, d.max()
