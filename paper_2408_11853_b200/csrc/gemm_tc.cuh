@@ -80,7 +80,10 @@ constexpr int GEMM_BK = 64;
 constexpr int GEMM_THREADS = 384;
 constexpr int GEMM_EPI_WARPS = 8;
 constexpr int GEMM_SMEM_LIMIT = 232448;  // 227 KB opt-in dynamic smem
-constexpr int GEMM_EPI_BYTES = GEMM_EPI_WARPS * 32 * 33 * 4;
+// per-warp transpose buffer: 32 rows x 32 floats, 16-byte chunks XOR-swizzled by
+// row (8 lanes writing or reading float4 hit 8 distinct bank quads)
+constexpr int GEMM_EPI_STRIDE = 32;
+constexpr int GEMM_EPI_BYTES = GEMM_EPI_WARPS * 32 * GEMM_EPI_STRIDE * 4;
 constexpr int GEMM_BAR_BYTES = 256;
 
 template <int BN, bool SPLIT>
@@ -135,14 +138,18 @@ __device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, in
     float v[32];
     tmem_ld_32x32(tacc + c, v);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = v[i];
+    for (int i = 0; i < 32; i += 4)
+      *reinterpret_cast<float4*>(buf + lane * GEMM_EPI_STRIDE + (((i >> 2) ^ (lane & 7)) << 2)) =
+          make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
     __syncwarp();
     const float4 b = *reinterpret_cast<const float4*>(args.bias + col);
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
       const int r = it * 4 + rs;
       if (r < rows) {
-        const float* src = buf + r * 33 + 4 * cg;
+        const float4 src4 =
+            *reinterpret_cast<const float4*>(buf + r * GEMM_EPI_STRIDE + ((cg ^ (r & 7)) << 2));
+        const float src[4] = {src4.x, src4.y, src4.z, src4.w};
         float x[4];
         if (args.r16) {
           x[0] = round16(round16(src[0]) + b.x); x[1] = round16(round16(src[1]) + b.y);
@@ -335,7 +342,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int ew = warp - 4;       // 0..7
     const int q = warp & 3;        // TMEM lane quarter == 32-row block of the tile
     const int half = ew >> 2;      // which alternate 32-column chunks this warp owns
-    float* buf = epi_buf + ew * 32 * 33;
+    float* buf = epi_buf + ew * 32 * GEMM_EPI_STRIDE;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -382,7 +389,7 @@ struct Gemm2Cfg {
   // gets 16 warps (4 per TMEM lane quarter) instead of 8
   static constexpr int EPI_WARPS = SPLIT ? 8 : 16;
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
-  static constexpr int EPI_BYTES = EPI_WARPS * 32 * 33 * 4;
+  static constexpr int EPI_BYTES = EPI_WARPS * 32 * GEMM_EPI_STRIDE * 4;
   static constexpr int NOPS = SPLIT ? 2 : 1;
   static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;  // this CTA's 128 rows
   static constexpr int B_BYTES = 128 * GEMM_BK * 2;      // this CTA's half of BN = 256
@@ -528,7 +535,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
     const int ew = warp - 4;       // 0..EPI_WARPS-1
     const int q = warp & 3;        // TMEM lane quarter == 32-row block of this CTA's half tile
     const int half = ew >> 2;      // which 32-column chunks (every EPI_WARPS/4-th) it owns
-    float* buf = epi_buf + ew * 32 * 33;
+    float* buf = epi_buf + ew * 32 * GEMM_EPI_STRIDE;
     const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
     int acc = 0;
     uint32_t acc_phase = 0;
