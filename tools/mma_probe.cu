@@ -21,13 +21,14 @@ __global__ void __launch_bounds__(128, 1) probe(long long* out, int mode, int N,
   tc_fence_before(); __syncthreads(); tc_fence_after();
   const uint32_t tm = slot;
   if (threadIdx.x == 0) {
-    const uint32_t idesc = idesc_f16kind(128, N, 0) | (mode == 1 ? (1u << 16) : 0u);
+    const uint32_t M = mode >= 2 ? 64 : 128;
+    const uint32_t idesc = idesc_f16kind(M, N, 0) | ((mode & 1) ? (1u << 16) : 0u);
     const uint64_t a = umma_desc_sw128(sm), b = umma_desc_sw128(sm + 32768);
     long long tot = 0;
     for (int r = 0; r < reps; ++r) {
       const long long t0 = clock64();
       for (int i = 0; i < nmma; ++i) {
-        if (mode == 0) tc_mma_bf16(tm, a + 2 * (i & 3), b + 2 * (i & 3), idesc, i != 0);
+        if (mode == 0 || mode == 2) tc_mma_bf16(tm, a + 2 * (i & 3), b + 2 * (i & 3), idesc, i != 0);
         else mma_ts(tm + 256, tm + 8 * (i % 16), b + 128 * (i % 8), idesc, i != 0);
       }
       tc_commit(&bar);
@@ -47,12 +48,14 @@ int main() {
     {0, 128, 1, "SS 128x128x16 x1"}, {0, 128, 12, "SS 128x128x16 x12"}, {0, 112, 12, "SS 128x112x16 x12"},
     {0, 64, 12, "SS 128x64x16 x12"}, {0, 256, 12, "SS 128x256x16 x12"}, {0, 256, 48, "SS 128x256x16 x48"},
     {0, 128, 48, "SS 128x128x16 x48"}, {1, 64, 1, "TS 128x64x16 x1"}, {1, 64, 21, "TS 128x64x16 x21"},
-    {1, 64, 48, "TS 128x64x16 x48"}, {1, 128, 21, "TS 128x128x16 x21"}, {1, 256, 21, "TS 128x256x16 x21"}};
+    {1, 64, 48, "TS 128x64x16 x48"}, {1, 128, 21, "TS 128x128x16 x21"}, {1, 256, 21, "TS 128x256x16 x21"},
+    {2, 64, 12, "SS 64x64x16 x12"}, {2, 128, 12, "SS 64x128x16 x12"}, {2, 256, 12, "SS 64x256x16 x12"},
+    {3, 64, 21, "TS 64x64x16 x21"}, {3, 128, 21, "TS 64x128x16 x21"}};
   for (auto& c : cases) {
     probe<<<148, 128, 100000>>>(d, c.mode, c.N, c.nmma, 64);
     cudaError_t e = cudaDeviceSynchronize();
     long long cyc = 0; cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
-    const double ideal = (double)c.nmma * 128.0 * c.N * 16 * 2 / 8192.0;
+    const double ideal = (double)c.nmma * (c.mode >= 2 ? 64.0 : 128.0) * c.N * 16 * 2 / 8192.0;
     printf("%-22s %s  %6lld cycles/batch  (ideal %6.0f, %.2fx)\n", c.what, e ? cudaGetErrorString(e) : "ok", cyc, ideal, cyc / ideal);
   }
   return 0;
