@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
         pair_sync();
         mx = fmaxf(mx, red_max[(hf ^ 1) * 128 + r]);
         const float mxc = mx * c2;
-        float sum = 0.f;
+        float2 sum2 = make_float2(0.f, 0.f);  // even / odd keys, summed at the end
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int c = hf + 2 * j;
@@ -444,19 +444,21 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
               if (in && e >= 32) {
 #pragma unroll
                 for (int i = 0; i < 16; i += 2) {
-                  const float p0 = fast_exp2(fmaf(v[half * 16 + i], c2, -mxc));
-                  const float p1 = fast_exp2(fmaf(v[half * 16 + i + 1], c2, -mxc));
-                  sum += p0 + p1;
+                  const float2 t = ffma2(make_float2(v[half * 16 + i], v[half * 16 + i + 1]),
+                                         make_float2(c2, c2), make_float2(-mxc, -mxc));
+                  const float p0 = fast_exp2(t.x), p1 = fast_exp2(t.y);
+                  sum2 = fadd2(sum2, make_float2(p0, p1));
                   split2(p0, p1, fmt, hh[i / 2], ll[i / 2]);
                 }
               } else if (in) {
                 const int eh = e - half * 16;
 #pragma unroll
                 for (int i = 0; i < 16; i += 2) {
-                  const float p0 = i < eh ? fast_exp2(fmaf(v[half * 16 + i], c2, -mxc)) : 0.f;
-                  const float p1 =
-                      i + 1 < eh ? fast_exp2(fmaf(v[half * 16 + i + 1], c2, -mxc)) : 0.f;
-                  sum += p0 + p1;
+                  const float2 t = ffma2(make_float2(v[half * 16 + i], v[half * 16 + i + 1]),
+                                         make_float2(c2, c2), make_float2(-mxc, -mxc));
+                  const float p0 = i < eh ? fast_exp2(t.x) : 0.f;
+                  const float p1 = i + 1 < eh ? fast_exp2(t.y) : 0.f;
+                  sum2 = fadd2(sum2, make_float2(p0, p1));
                   split2(p0, p1, fmt, hh[i / 2], ll[i / 2]);
                 }
               } else {
@@ -469,7 +471,7 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
           }
         }
         tc_wait_st();
-        red_sum[hf * 128 + r] = sum;
+        red_sum[hf * 128 + r] = sum2.x + sum2.y;
         pair_sync();
       }
       tc_fence_before();

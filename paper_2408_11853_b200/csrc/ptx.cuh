@@ -278,6 +278,26 @@ __device__ __forceinline__ bool split16(float v, int fmt, uint16_t& hi, uint16_t
   lo = __bfloat16_as_ushort(__float2bfloat16_rn(v - __bfloat162float(h)));
   return true;
 }
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2: two lanes of fp32 math per instruction).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
 // Two values -> packed (hi, lo) 16-bit pairs (element a in the low half), no
 // range check: for values already known to be inside the fp16 range (softmax
 // weights in [0, 1], convex combinations of range-checked values).
@@ -285,7 +305,8 @@ __device__ __forceinline__ void split2(float a, float b, int fmt, uint32_t& hi, 
   if (fmt == FMT_F16) {
     const __half2 h = __floats2half2_rn(a, b);
     const float2 f = __half22float2(h);
-    const __half2 l = __floats2half2_rn(a - f.x, b - f.y);
+    const float2 r = fadd2(make_float2(a, b), make_float2(-f.x, -f.y));
+    const __half2 l = __floats2half2_rn(r.x, r.y);
     hi = *reinterpret_cast<const uint32_t*>(&h);
     lo = *reinterpret_cast<const uint32_t*>(&l);
   } else {
