@@ -155,7 +155,9 @@ __device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, in
           x[0] = round16(round16(src[0]) + b.x); x[1] = round16(round16(src[1]) + b.y);
           x[2] = round16(round16(src[2]) + b.z); x[3] = round16(round16(src[3]) + b.w);
         } else {
-          x[0] = src[0] + b.x; x[1] = src[1] + b.y; x[2] = src[2] + b.z; x[3] = src[3] + b.w;
+          const float2 x01 = fadd2(make_float2(src[0], src[1]), make_float2(b.x, b.y));
+          const float2 x23 = fadd2(make_float2(src[2], src[3]), make_float2(b.z, b.w));
+          x[0] = x01.x; x[1] = x01.y; x[2] = x23.x; x[3] = x23.y;
         }
         const size_t o = (size_t)(row0 + r);
         if (EPI == EPI_F32 || EPI == EPI_F32_RES) {
@@ -188,10 +190,14 @@ __device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, in
           }
         } else {
           float y[4];
+          if (EPI == EPI_GELU_SPLIT) {
+            const float2 y01 = gelu_tanh2(make_float2(x[0], x[1]));
+            const float2 y23 = gelu_tanh2(make_float2(x[2], x[3]));
+            y[0] = y01.x; y[1] = y01.y; y[2] = y23.x; y[3] = y23.y;
+          } else {
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            y[j] = (EPI == EPI_GELU_SPLIT) ? gelu_tanh(x[j])
-                   : (EPI == EPI_TANH_SPLIT) ? tanhf(x[j]) : x[j];
+            for (int j = 0; j < 4; ++j) y[j] = (EPI == EPI_TANH_SPLIT) ? tanhf(x[j]) : x[j];
+          }
           // fp16 range: |y| >= 65520 rounds to inf (binary16 overflow) -> flag
           if (args.fmt == FMT_F16 && args.ovf &&
               fmaxf(fmaxf(fabsf(y[0]), fabsf(y[1])), fmaxf(fabsf(y[2]), fabsf(y[3]))) >= 65520.f)

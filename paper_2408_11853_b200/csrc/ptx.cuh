@@ -298,6 +298,16 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return d;
 }
 
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
 // Two values -> packed (hi, lo) 16-bit pairs (element a in the low half), no
 // range check: for values already known to be inside the fp16 range (softmax
 // weights in [0, 1], convex combinations of range-checked values).
@@ -345,6 +355,17 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   const float c2 = -2.0f * 0.7978845608028654f * 1.4426950408889634f;  // -2 sqrt(2/pi) log2(e)
   const float e = fminf(fast_exp2(c2 * (x + 0.044715f * x * x * x)), 1e30f);
   return __fdividef(x, 1.0f + e);
+}
+
+// gelu_tanh on a pair with packed fp32 math (same operation order as gelu_tanh)
+__device__ __forceinline__ float2 gelu_tanh2(float2 x) {
+  const float c2 = -2.0f * 0.7978845608028654f * 1.4426950408889634f;
+  const float2 x2 = fmul2(x, x);
+  const float2 x3 = fmul2(x2, x);
+  const float2 z = fmul2(make_float2(c2, c2), ffma2(make_float2(0.044715f, 0.044715f), x3, x));
+  const float e0 = fminf(fast_exp2(z.x), 1e30f), e1 = fminf(fast_exp2(z.y), 1e30f);
+  const float2 den = fadd2(make_float2(1.0f, 1.0f), make_float2(e0, e1));
+  return make_float2(__fdividef(x.x, den.x), __fdividef(x.y, den.y));
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

@@ -91,7 +91,8 @@ def gpu():
     global _gpu
     with _lock:
         if _gpu is None:
-            lib = _load("libmfgpu.so")
+            # MFG_GPU_LIB selects another build in lib/ (same-box A/B timing runs)
+            lib = _load(os.environ.get("MFG_GPU_LIB", "libmfgpu.so"))
             lib.mfg_create.argtypes = [C.POINTER(MfgConfig), C.POINTER(C.c_void_p)]
             lib.mfg_create.restype = C.c_int
             lib.mfg_score_batch.argtypes = [C.c_void_p, i32, i32, i32p, i64p, f32p]
