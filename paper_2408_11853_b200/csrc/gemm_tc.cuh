@@ -7,7 +7,7 @@
 // and fuses the ops that follow each affine into the epilogue:
 //   EPI_F32        out = acc + bias                         (QKV, head output)
 //   EPI_F32_RES    out = acc + bias + residual              (O-proj, FFN2)
-//   EPI_GELU_SPLIT out = gelu_tanh(acc + bias) -> hi/lo pieces (FFN1, `encoder.py:149-151`)
+//   EPI_GELU_SPLIT out = gelu_tanh2(acc + bias) -> hi/lo pieces (FFN1, `encoder.py:149-151`)
 //   EPI_TANH_SPLIT out = tanh(acc + bias)      -> hi/lo pieces (head hidden stages, `:190-196`)
 //   EPI_SPLIT      out = acc + bias            -> hi/lo pieces (Q|K|V for attention)
 //

@@ -48,18 +48,6 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 #endif
   return ok != 0;
 }
-// Non-blocking probe of a phase (for event-loop style issuers).
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
 // Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
 // try_wait carries a suspend-time hint, so a waiting warp sleeps in hardware
 // until the phase flips instead of spinning on issue slots its neighbours need.
@@ -347,17 +335,11 @@ __device__ __forceinline__ float load16(const uint16_t* p, size_t i, int fmt) {
 }
 
 // gelu_tanh(x) = 0.5 x (1 + tanh(z)), z = sqrt(2/pi) (x + 0.044715 x^3)
-// (`encoder.py:47-49`), evaluated as the algebraically identical x / (1 + e^{-2z}):
-// one MUFU.EX2 and one fast division instead of tanhf's ~25-instruction path,
-// no cancellation for negative x, relative error a few fp32 ulp. e^{-2z} is
-// clamped so the division never sees an infinite denominator.
-__device__ __forceinline__ float gelu_tanh(float x) {
-  const float c2 = -2.0f * 0.7978845608028654f * 1.4426950408889634f;  // -2 sqrt(2/pi) log2(e)
-  const float e = fminf(fast_exp2(c2 * (x + 0.044715f * x * x * x)), 1e30f);
-  return __fdividef(x, 1.0f + e);
-}
-
-// gelu_tanh on a pair with packed fp32 math (same operation order as gelu_tanh)
+// (`encoder.py:47-49`), evaluated as the algebraically identical x / (1 + e^{-2z})
+// on a pair with packed fp32 math: MUFU.EX2 and a fast division instead of
+// tanhf's ~25-instruction path, no cancellation for negative x, relative error a
+// few fp32 ulp; e^{-2z} is clamped so the division never sees an infinite
+// denominator.
 __device__ __forceinline__ float2 gelu_tanh2(float2 x) {
   const float c2 = -2.0f * 0.7978845608028654f * 1.4426950408889634f;
   const float2 x2 = fmul2(x, x);
