@@ -111,6 +111,16 @@ __device__ __forceinline__ void tmem_ld_32x8(uint32_t taddr, float (&v)[8]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
+// 16 consecutive fp32 columns of this warp's lanes, without waiting (tc_wait_ld)
+__device__ __forceinline__ void tmem_ld_raw16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_st_1(uint32_t taddr, uint32_t v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
 }
@@ -487,13 +497,17 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
         const size_t ob = (size_t)(t0 + r - ks) * ldc + h * DH + hf * 32;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
+          // both O pieces of this half in flight together, one wait
+          uint32_t ov[16], ow[16];
+          tmem_ld_raw16(to + half * 16, ov);
+          if (SPLIT && !TAIL) tmem_ld_raw16(to + 64 + half * 16, ow);
+          tc_wait_ld();
           float v[16];
-          tmem_ld_32x16(to + half * 16, v);
-          if (SPLIT && !TAIL) {  // O = Ph·Vh + Pl·Vh (columns 0..63) + Ph·Vl (64..127)
-            float w[16];
-            tmem_ld_32x16(to + 64 + half * 16, w);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += w[i];
+          for (int i = 0; i < 16; ++i) {
+            v[i] = __uint_as_float(ov[i]);
+            // O = Ph·Vh + Pl·Vh (columns 0..63) + Ph·Vl (64..127)
+            if (SPLIT && !TAIL) v[i] += __uint_as_float(ow[i]);
           }
           if (r < ke) {
             // ctx is a convex combination of range-checked V rows: no fp16 overflow;
