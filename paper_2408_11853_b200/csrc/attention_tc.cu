@@ -35,8 +35,9 @@
 //   warps 2-9    group 0 (items k even, TMEM region 0): softmax, then epilogue
 //   warps 10-17  group 1 (items k odd,  TMEM region 1)
 // Inside a group two warps share each TMEM lane quarter (= 32 tile rows): warp
-// half hf takes the key chunks c with c % 2 == hf and the O columns 32hf..+31;
-// the pair exchanges row max / row sum through TMEM (named barrier).
+// hr takes rows 16hr..16hr+15 of it through the 16x32bx2 TMEM shape (lanes 0-15
+// even key chunks / O columns 0..31, lanes 16-31 odd chunks / columns 32..63), so
+// row max and row sum combine with one warp shuffle.
 // TMEM columns: S/P of region b at 128b..128b+127; O of region b at 256+128b
 // (MODE 3: Ph·Vh + Pl·Vh in the first 64 columns, Ph·Vl in the next 64).
 // Measured (tools/mma_probe.cu): a 128xNx16 MMA costs >= ~72 cycles (SS) /
@@ -70,9 +71,8 @@ struct AtqCfg {
   static constexpr int QK_BYTES = NPL_QK * (ATQ_TILE + (TAIL ? ATQ_TTILE : 0));
   static constexpr int V_BYTES = NPL_V * (ATQ_TILE + (TAIL ? ATQ_TTILE : 0));
   static constexpr int QK_ST = SPLIT ? 2 : 3;
-  static constexpr int V_ST = SPLIT ? (TAIL ? 1 : 2) : (TAIL ? 3 : 5);
-  static constexpr int RED_OFF = QK_ST * QK_BYTES + V_ST * V_BYTES;  // [group][max|sum][half][row]
-  static constexpr int BAR_OFF = RED_OFF + 2 * 2 * 2 * 128 * 4;
+  static constexpr int V_ST = SPLIT ? (TAIL ? 1 : 3) : (TAIL ? 3 : 5);
+  static constexpr int BAR_OFF = QK_ST * QK_BYTES + V_ST * V_BYTES;
   static constexpr int SMEM = 1024 + BAR_OFF + 256;
   static_assert(SMEM <= 232448, "attention smem");
 };
@@ -120,6 +120,42 @@ __device__ __forceinline__ void tmem_ld_raw16(uint32_t taddr, uint32_t (&r)[16])
         "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
         "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
+}
+// 16x32bx2 shape: lanes 0-15 of the warp access TMEM lanes base+0..15 at columns
+// [c, c+N), lanes 16-31 the same TMEM lanes at columns [c+N, c+2N) (split offset N).
+__device__ __forceinline__ void tmem_ld_16x32bx2(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], 32;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld_16x32bx2_8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], 8;"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+// 8 columns per lane at c (lanes 0-15) and c+32 (lanes 16-31)
+__device__ __forceinline__ void tmem_st_16x32bx2_8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x32bx2.x8.b32 [%0], 32, {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+      : "memory");
 }
 __device__ __forceinline__ void tmem_st_1(uint32_t taddr, uint32_t v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
@@ -377,24 +413,25 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
     }
   } else if (warp < 18) {
     // ------------------------------------------------------------ softmax + epilogue
+    // Warp (q, hr) of a group owns tile rows 32q + 16hr .. +15 (TMEM lane quarter
+    // q, lane half hr). With the 16x32bx2 TMEM shape, lanes 0-15 of the warp read
+    // key chunk 2j and lanes 16-31 chunk 2j+1 of the same 16 rows, so the row max
+    // and row sum combine with one shuffle (no cross-warp exchange).
     const int g = (warp - 2) >> 3;          // group = region = item parity
-    const int hf = ((warp - 2) >> 2) & 1;   // which half of the key chunks
+    const int hr = ((warp - 2) >> 2) & 1;   // which 16 rows of the quarter
     const int q = warp & 3;                 // TMEM lane quarter
-    const int r = q * 32 + lane;            // tile row owned by this thread
-    const int pair_bar = 1 + g * 4 + q;     // named barrier of the two warps of this quarter
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    float* red_max = reinterpret_cast<float*>(sm + C::RED_OFF) + g * 512;  // [half][row]
-    float* red_sum = red_max + 256;
+    const int cp = lane >> 4;               // chunk parity this thread handles
+    const int r = q * 32 + hr * 16 + (lane & 15);  // tile row owned by this thread
+    const uint32_t lane_off = (uint32_t)(q * 32 + hr * 16) << 16;
     const float c2 = scale * 1.4426950408889634f;  // exp(x*scale) = 2^(x*c2)
-    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
     for (int k = g; k < mine; k += 2) {
       const int b = g;
       const int it = item_of(k);
       const AttTile tl = tiles[it / heads];
       const int h = it % heads;
       const int n16 = (att_tile_rows(tl) + 15) & ~15;
-      // The 32 rows of this warp are one 32-row granule, i.e. (part of) exactly
-      // one sequence slot: its keys are [ks, ke) of the tile (warp-uniform).
+      // This warp's rows lie in one 32-row granule = (part of) one sequence
+      // slot: its keys are [ks, ke) of the tile (warp-uniform).
       int ks = 0, ke = 0, t0 = 0;
       {
         int o = 0;
@@ -409,45 +446,46 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
           o += R;
         }
       }
-      const bool active = ke > ks;
+      const bool active = ke > q * 32 + hr * 16;  // some row of this warp is real
       mbar_wait(&s_full[b], (k >> 1) & 1);
-      const bool tr = hf == 0 && q == 0 && lane == 0;
+      const bool tr = hr == 0 && q == 0 && lane == 0;
       if (tr) ATT_TRACE(k, 2);
       tc_fence_after();
+      float rsum = 1.f;
       if (active) {
         const uint32_t trow = tm + b * 128 + lane_off;
         const int c_lo = ks >> 5, c_hi = (ke - 1) >> 5, c_end = (n16 + 31) >> 5;
         float mx = -INFINITY;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const int c = hf + 2 * j;
-          if (c >= c_lo && c <= c_hi) {
+          if (2 * j + 1 >= c_lo && 2 * j <= c_hi) {  // warp-uniform: the pair has keys
             float v[32];
-            tmem_ld_32x32(trow + c * 32, v);
-            const int e = ke - c * 32;  // keys i < e of this chunk are the sequence's
-            if (e >= 32) {
+            tmem_ld_16x32bx2(trow + j * 64, v);
+            const int c = 2 * j + cp;
+            if (c >= c_lo && c <= c_hi) {
+              const int e = ke - c * 32;
+              if (e >= 32) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i) mx = fmaxf(mx, v[i]);
-            } else {
+                for (int i = 0; i < 32; ++i) mx = fmaxf(mx, v[i]);
+              } else {
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (i < e) mx = fmaxf(mx, v[i]);
+                for (int i = 0; i < 32; ++i)
+                  if (i < e) mx = fmaxf(mx, v[i]);
+              }
             }
           }
         }
-        red_max[hf * 128 + r] = mx;
-        pair_sync();
-        mx = fmaxf(mx, red_max[(hf ^ 1) * 128 + r]);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
         const float mxc = mx * c2;
         float2 sum2 = make_float2(0.f, 0.f);  // even / odd keys, summed at the end
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const int c = hf + 2 * j;
-          if (c < c_end) {
+          if (2 * j < c_end) {  // warp-uniform
+            const int c = 2 * j + cp;
             const bool in = c >= c_lo && c <= c_hi;
             const int e = ke - c * 32;
             float v[32];
-            if (in) tmem_ld_32x32(trow + c * 32, v);
+            tmem_ld_16x32bx2(trow + j * 64, v);
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
               uint32_t hh[8], ll[8];
@@ -475,58 +513,56 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
 #pragma unroll
                 for (int i = 0; i < 8; ++i) hh[i] = ll[i] = 0u;
               }
-              tmem_st_8(trow + c * 32 + half * 8, hh);
-              if (PSPLIT) tmem_st_8(trow + c * 32 + 16 + half * 8, ll);
+              // lanes 0-15 -> chunk 2j, lanes 16-31 -> chunk 2j+1 (32 columns on)
+              tmem_st_16x32bx2_8(trow + j * 64 + half * 8, hh);
+              if (PSPLIT) tmem_st_16x32bx2_8(trow + j * 64 + 16 + half * 8, ll);
             }
           }
         }
         tc_wait_st();
-        red_sum[hf * 128 + r] = sum2.x + sum2.y;
-        pair_sync();
+        rsum = sum2.x + sum2.y;
+        rsum += __shfl_xor_sync(0xffffffffu, rsum, 16);
       }
       tc_fence_before();
       mbar_arrive(&p_full[b]);
       if (tr) ATT_TRACE(k, 3);
-      // ---- epilogue: O columns 32hf..32hf+31 / rowsum -> ctx pieces
+      // ---- epilogue: lanes 0-15 O columns 0..31, lanes 16-31 columns 32..63
       mbar_wait(&o_full[b], (k >> 1) & 1);
       if (tr) ATT_TRACE(k, 4);
       tc_fence_after();
       if (active) {
-        const uint32_t to = tm + lane_off + 256 + b * 128 + hf * 32;
-        const float inv = 1.0f / (red_sum[r] + red_sum[128 + r]);
-        const size_t ob = (size_t)(t0 + r - ks) * ldc + h * DH + hf * 32;
+        const uint32_t to = tm + lane_off + 256 + b * 128;
+        const float inv = 1.0f / rsum;
+        const size_t ob = (size_t)(t0 + r - ks) * ldc + h * DH + cp * 32;
+        float v[32];
+        tmem_ld_16x32bx2(to, v);
+        if (SPLIT && !TAIL) {  // O = Ph·Vh + Pl·Vh (columns 0..63) + Ph·Vl (64..127)
+          float w[32];
+          tmem_ld_16x32bx2(to + 64, w);
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          // both O pieces of this half in flight together, one wait
-          uint32_t ov[16], ow[16];
-          tmem_ld_raw16(to + half * 16, ov);
-          if (SPLIT && !TAIL) tmem_ld_raw16(to + 64 + half * 16, ow);
-          tc_wait_ld();
-          float v[16];
+          for (int i = 0; i < 32; ++i) v[i] += w[i];
+        }
+        if (r < ke) {
+          // ctx is a convex combination of range-checked V rows: no fp16 overflow;
+          // 16 pieces = 32 bytes per plane -> one 256-bit store each
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            v[i] = __uint_as_float(ov[i]);
-            // O = Ph·Vh + Pl·Vh (columns 0..63) + Ph·Vl (64..127)
-            if (SPLIT && !TAIL) v[i] += __uint_as_float(ow[i]);
-          }
-          if (r < ke) {
-            // ctx is a convex combination of range-checked V rows: no fp16 overflow;
-            // 16 pieces = 32 bytes per plane -> one 256-bit store each
+          for (int half = 0; half < 2; ++half) {
             uint32_t hh[8], ll[8];
 #pragma unroll
-            for (int i = 0; i < 16; i += 2) split2(v[i] * inv, v[i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
+            for (int i = 0; i < 16; i += 2)
+              split2(v[half * 16 + i] * inv, v[half * 16 + i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
             st_global_256(ch + ob + half * 16, hh);
             if (SPLIT) st_global_256(cl + ob + half * 16, ll);
           }
         }
-        if (TAIL) {  // head dims 64..79: columns 64 + 8hf .. +7
-          float v[8];
-          tmem_ld_32x8(tm + lane_off + 256 + b * 128 + 64 + hf * 8, v);
+        if (TAIL) {  // head dims 64..79: lanes 0-15 dims 64..71, lanes 16-31 dims 72..79
+          float t8[8];
+          tmem_ld_16x32bx2_8(tm + lane_off + 256 + b * 128 + 64, t8);
           if (r < ke) {
             uint32_t hh[4], ll[4];
 #pragma unroll
-            for (int i = 0; i < 8; i += 2) split2(v[i] * inv, v[i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
-            const size_t ot = (size_t)(t0 + r - ks) * ldc + h * DH + 64 + hf * 8;
+            for (int i = 0; i < 8; i += 2) split2(t8[i] * inv, t8[i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
+            const size_t ot = (size_t)(t0 + r - ks) * ldc + h * DH + 64 + cp * 8;
             *reinterpret_cast<uint4*>(ch + ot) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
             if (SPLIT) *reinterpret_cast<uint4*>(cl + ot) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
           }
