@@ -26,6 +26,8 @@
 // overlap the MMAs of tile i+1. Tiles are assigned round-robin to a persistent
 // grid of <= #SM CTAs.
 #pragma once
+#include <type_traits>
+
 #include "ptx.cuh"
 
 namespace mfg {
@@ -103,23 +105,36 @@ struct GemmCfg {
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
 };
 
+__device__ __forceinline__ __half2 u2h2(uint32_t u) { return *reinterpret_cast<const __half2*>(&u); }
+__device__ __forceinline__ uint32_t h22u(__half2 h) { return *reinterpret_cast<const uint32_t*>(&h); }
+
 // One accumulator tile's epilogue for one warp: TMEM lanes = tile rows
 // row0..row0+rows-1 (this warp's quarter), every other 32-column chunk starting
 // at `half`*32; each chunk transposed through `buf` so global traffic is float4
 // per lane, 4 full 128-byte row segments per warp instruction.
-template <int BN, int EPI, int NSUB = 2>
-__device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, int row0, int rows,
-                                         int n0, int half, float* buf, int lane) {
+// FMT / R16 are the run-time `args.fmt` / `args.r16` hoisted to compile time.
+// R16 (reference binary16 mode, `encoder.py:120-126`): the product is rounded to
+// binary16 and the (binary16) bias added in binary16; both are exact IEEE binary16
+// operations, done as packed __hadd2 (an fp32 sum of two binary16 values rounded
+// once to binary16 is the correctly rounded binary16 sum, so this equals
+// round16(round16(acc) + b)); with a binary16 residual and output the residual
+// sum is one more __hadd2.
+template <int BN, int EPI, int NSUB, int FMT, bool R16>
+__device__ __forceinline__ void epi_tile_t(const GemmArgs& args, uint32_t tacc, int row0, int rows,
+                                           int n0, int half, float* buf, int lane) {
   const int cg = lane & 7;       // transposed phase: 4 columns 4*cg..4*cg+3
   const int rs = lane >> 3;      // row sub-index 0..3
-  if (rows <= 0) return;         // warp-uniform: this quarter of the tile is past M
+  const bool r16res = EPI == EPI_F32_RES && args.res_hi != nullptr;
+  const bool h16 = R16 && r16res && args.res_lo == nullptr && args.out16 != nullptr;
+  constexpr bool SPLIT_OUT = EPI == EPI_GELU_SPLIT || EPI == EPI_TANH_SPLIT || EPI == EPI_SPLIT;
+  float amax = 0.f;  // largest |output| (fp16 overflow flag, split epilogues)
+  uint32_t hinf = 0;  // R16 EPI_SPLIT: bit 15/31 set when a binary16 output is inf
 #pragma unroll 1
   for (int c = half * 32; c < BN; c += 32 * NSUB) {
     const int col = n0 + c + 4 * cg;
     // prefetch this chunk's residual (8 x float4, or 8 x (hi, lo) 4 x 16-bit
     // pieces per lane) before touching TMEM; converted where it is consumed
     uint4 rraw[8];  // float4 bits, or {hi pieces x2, lo pieces x2}
-    const bool r16res = EPI == EPI_F32_RES && args.res_hi != nullptr;
     if (EPI == EPI_F32_RES) {
 #pragma unroll
       for (int it = 0; it < 8; ++it) {
@@ -143,85 +158,111 @@ __device__ __forceinline__ void epi_tile(const GemmArgs& args, uint32_t tacc, in
           make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
     __syncwarp();
     const float4 b = *reinterpret_cast<const float4*>(args.bias + col);
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
+    const __half2 bh01 = __floats2half2_rn(b.x, b.y), bh23 = __floats2half2_rn(b.z, b.w);
+    auto row = [&](int it) {
       const int r = it * 4 + rs;
-      if (r < rows) {
-        const float4 src4 =
-            *reinterpret_cast<const float4*>(buf + r * GEMM_EPI_STRIDE + ((cg ^ (r & 7)) << 2));
-        const float src[4] = {src4.x, src4.y, src4.z, src4.w};
-        float x[4];
-        if (args.r16) {
-          x[0] = round16(round16(src[0]) + b.x); x[1] = round16(round16(src[1]) + b.y);
-          x[2] = round16(round16(src[2]) + b.z); x[3] = round16(round16(src[3]) + b.w);
-        } else {
-          const float2 x01 = fadd2(make_float2(src[0], src[1]), make_float2(b.x, b.y));
-          const float2 x23 = fadd2(make_float2(src[2], src[3]), make_float2(b.z, b.w));
-          x[0] = x01.x; x[1] = x01.y; x[2] = x23.x; x[3] = x23.y;
+      const float4 s4 =
+          *reinterpret_cast<const float4*>(buf + r * GEMM_EPI_STRIDE + ((cg ^ (r & 7)) << 2));
+      const size_t o = (size_t)(row0 + r);
+      float2 x01, x23;
+      if (R16) {
+        __half2 h01 = __hadd2(__floats2half2_rn(s4.x, s4.y), bh01);
+        __half2 h23 = __hadd2(__floats2half2_rn(s4.z, s4.w), bh23);
+        if (EPI == EPI_F32_RES && h16) {
+          h01 = __hadd2(h01, u2h2(rraw[it].x));
+          h23 = __hadd2(h23, u2h2(rraw[it].y));
+          *reinterpret_cast<uint2*>(args.out16 + o * args.ldo + col) =
+              make_uint2(h22u(h01), h22u(h23));
+          return;
         }
-        const size_t o = (size_t)(row0 + r);
-        if (EPI == EPI_F32 || EPI == EPI_F32_RES) {
-          if (EPI == EPI_F32_RES) {
-            float4 res;
-            if (r16res) {
-              const uint16_t* h = reinterpret_cast<const uint16_t*>(&rraw[it].x);
-              const uint16_t* l = reinterpret_cast<const uint16_t*>(&rraw[it].z);
-              res = make_float4(load16(h, 0, args.fmt) + load16(l, 0, args.fmt),
-                                load16(h, 1, args.fmt) + load16(l, 1, args.fmt),
-                                load16(h, 2, args.fmt) + load16(l, 2, args.fmt),
-                                load16(h, 3, args.fmt) + load16(l, 3, args.fmt));
-            } else {
-              res = make_float4(__uint_as_float(rraw[it].x), __uint_as_float(rraw[it].y),
-                                __uint_as_float(rraw[it].z), __uint_as_float(rraw[it].w));
-            }
-            x[0] += res.x; x[1] += res.y; x[2] += res.z; x[3] += res.w;
-            if (args.r16) {
-              x[0] = round16(x[0]); x[1] = round16(x[1]); x[2] = round16(x[2]); x[3] = round16(x[3]);
-            }
-          }
-          if (args.out16) {
-            const __half2 a = __floats2half2_rn(x[0], x[1]), b2 = __floats2half2_rn(x[2], x[3]);
-            *reinterpret_cast<uint2*>(args.out16 + o * args.ldo + col) =
-                make_uint2(*reinterpret_cast<const uint32_t*>(&a),
-                           *reinterpret_cast<const uint32_t*>(&b2));
-          } else {
-            *reinterpret_cast<float4*>(args.out_f32 + o * args.ldo + col) =
-                make_float4(x[0], x[1], x[2], x[3]);
-          }
-        } else {
-          float y[4];
-          if (EPI == EPI_GELU_SPLIT) {
-            const float2 y01 = gelu_tanh2(make_float2(x[0], x[1]));
-            const float2 y23 = gelu_tanh2(make_float2(x[2], x[3]));
-            y[0] = y01.x; y[1] = y01.y; y[2] = y23.x; y[3] = y23.y;
-          } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) y[j] = (EPI == EPI_TANH_SPLIT) ? tanhf(x[j]) : x[j];
-          }
-          // fp16 range: |y| >= 65520 rounds to inf (binary16 overflow) -> flag
-          if (args.fmt == FMT_F16 && args.ovf &&
-              fmaxf(fmaxf(fabsf(y[0]), fabsf(y[1])), fmaxf(fabsf(y[2]), fabsf(y[3]))) >= 65520.f)
-            atomicOr(args.ovf, 1);
-          uint32_t h01, h23, l01, l23;
-          if (args.out_lo) {
-            split2(y[0], y[1], args.fmt, h01, l01);
-            split2(y[2], y[3], args.fmt, h23, l23);
-            *reinterpret_cast<uint2*>(args.out_lo + o * args.ldh + col) = make_uint2(l01, l23);
-          } else if (args.fmt == FMT_F16) {
-            const __half2 a = __floats2half2_rn(y[0], y[1]), c = __floats2half2_rn(y[2], y[3]);
-            h01 = *reinterpret_cast<const uint32_t*>(&a);
-            h23 = *reinterpret_cast<const uint32_t*>(&c);
-          } else {
-            const __nv_bfloat162 a = __floats2bfloat162_rn(y[0], y[1]),
-                                 c = __floats2bfloat162_rn(y[2], y[3]);
-            h01 = *reinterpret_cast<const uint32_t*>(&a);
-            h23 = *reinterpret_cast<const uint32_t*>(&c);
-          }
-          *reinterpret_cast<uint2*>(args.out_hi + o * args.ldh + col) = make_uint2(h01, h23);
+        if (EPI == EPI_SPLIT && args.out_lo == nullptr) {  // the sums are the output
+          const uint32_t u01 = h22u(h01), u23 = h22u(h23);
+          // |h| >= 0x7c00 (inf) sets bit 15 of its half after + 0x0400 (no carry out)
+          hinf |= ((u01 & 0x7fff7fffu) + 0x04000400u) | ((u23 & 0x7fff7fffu) + 0x04000400u);
+          *reinterpret_cast<uint2*>(args.out_hi + o * args.ldh + col) = make_uint2(u01, u23);
+          return;
         }
+        x01 = __half22float2(h01);
+        x23 = __half22float2(h23);
+      } else {
+        x01 = fadd2(make_float2(s4.x, s4.y), make_float2(b.x, b.y));
+        x23 = fadd2(make_float2(s4.z, s4.w), make_float2(b.z, b.w));
       }
-    }
+      if (EPI == EPI_F32 || EPI == EPI_F32_RES) {
+        if (EPI == EPI_F32_RES) {
+          float2 r01, r23;
+          if (r16res) {
+            const uint16_t* h = reinterpret_cast<const uint16_t*>(&rraw[it].x);
+            const uint16_t* l = reinterpret_cast<const uint16_t*>(&rraw[it].z);
+            r01 = make_float2(load16(h, 0, FMT) + load16(l, 0, FMT), load16(h, 1, FMT) + load16(l, 1, FMT));
+            r23 = make_float2(load16(h, 2, FMT) + load16(l, 2, FMT), load16(h, 3, FMT) + load16(l, 3, FMT));
+          } else {
+            r01 = make_float2(__uint_as_float(rraw[it].x), __uint_as_float(rraw[it].y));
+            r23 = make_float2(__uint_as_float(rraw[it].z), __uint_as_float(rraw[it].w));
+          }
+          x01 = fadd2(x01, r01);
+          x23 = fadd2(x23, r23);
+          if (R16) {
+            x01 = make_float2(round16(x01.x), round16(x01.y));
+            x23 = make_float2(round16(x23.x), round16(x23.y));
+          }
+        }
+        if (args.out16) {
+          *reinterpret_cast<uint2*>(args.out16 + o * args.ldo + col) =
+              make_uint2(h22u(__floats2half2_rn(x01.x, x01.y)), h22u(__floats2half2_rn(x23.x, x23.y)));
+        } else {
+          *reinterpret_cast<float4*>(args.out_f32 + o * args.ldo + col) =
+              make_float4(x01.x, x01.y, x23.x, x23.y);
+        }
+      } else {
+        float2 y01 = x01, y23 = x23;
+        if (EPI == EPI_GELU_SPLIT) {
+          y01 = gelu_tanh2(x01);
+          y23 = gelu_tanh2(x23);
+        } else if (EPI == EPI_TANH_SPLIT) {
+          y01 = make_float2(tanhf(x01.x), tanhf(x01.y));
+          y23 = make_float2(tanhf(x23.x), tanhf(x23.y));
+        }
+        // fp16 range: |y| >= 65520 rounds to inf (binary16 overflow) -> flag below
+        if (FMT == FMT_F16)
+          amax = fmaxf(amax, fmaxf(fmaxf(fabsf(y01.x), fabsf(y01.y)), fmaxf(fabsf(y23.x), fabsf(y23.y))));
+        uint32_t h01, h23, l01, l23;
+        if (args.out_lo) {
+          split2(y01.x, y01.y, FMT, h01, l01);
+          split2(y23.x, y23.y, FMT, h23, l23);
+          *reinterpret_cast<uint2*>(args.out_lo + o * args.ldh + col) = make_uint2(l01, l23);
+        } else if (FMT == FMT_F16) {
+          h01 = h22u(__floats2half2_rn(y01.x, y01.y));
+          h23 = h22u(__floats2half2_rn(y23.x, y23.y));
+        } else {
+          const __nv_bfloat162 a = __floats2bfloat162_rn(y01.x, y01.y),
+                               c2 = __floats2bfloat162_rn(y23.x, y23.y);
+          h01 = *reinterpret_cast<const uint32_t*>(&a);
+          h23 = *reinterpret_cast<const uint32_t*>(&c2);
+        }
+        *reinterpret_cast<uint2*>(args.out_hi + o * args.ldh + col) = make_uint2(h01, h23);
+      }
+    };
+#pragma unroll
+    for (int it = 0; it < 8; ++it)
+      if (it * 4 + rs < rows) row(it);
     __syncwarp();
+  }
+  if (SPLIT_OUT && FMT == FMT_F16 && args.ovf && (amax >= 65520.f || (hinf & 0x80008000u)))
+    atomicOr(args.ovf, 1);
+}
+
+// Calls f(integral_constant<FMT>, bool_constant<R16>) for the run-time format:
+// the epilogue loop is instantiated once per combination (r16 implies fp16).
+template <class F>
+__device__ __forceinline__ void epi_dispatch(const GemmArgs& args, F&& f) {
+  if (args.fmt == FMT_F16) {
+    if (args.r16)
+      f(std::integral_constant<int, FMT_F16>{}, std::true_type{});
+    else
+      f(std::integral_constant<int, FMT_F16>{}, std::false_type{});
+  } else {
+    f(std::integral_constant<int, FMT_BF16>{}, std::false_type{});
   }
 }
 
@@ -349,25 +390,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int q = warp & 3;        // TMEM lane quarter == 32-row block of the tile
     const int half = ew >> 2;      // which alternate 32-column chunks this warp owns
     float* buf = epi_buf + ew * 32 * GEMM_EPI_STRIDE;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      int mt, nt;
-      tile_mn(tile, num_m, num_n, args.group_m, mt, nt);
-      const int m0 = mt * GEMM_BM;
-      const int n0 = nt * BN;
-      const int row0 = m0 + q * 32;
-      const int rows = min(32, args.M - row0);
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      epi_tile<BN, EPI>(args, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, row0, rows, n0,
-                        half, buf, lane);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
-    }
+    epi_dispatch(args, [&](auto fmt_c, auto r16_c) {
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        int mt, nt;
+        tile_mn(tile, num_m, num_n, args.group_m, mt, nt);
+        const int m0 = mt * GEMM_BM;
+        const int n0 = nt * BN;
+        const int row0 = m0 + q * 32;
+        const int rows = min(32, args.M - row0);
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        if (rows > 0)
+          epi_tile_t<BN, EPI, 2, decltype(fmt_c)::value, decltype(r16_c)::value>(
+              args, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, row0, rows, n0, half, buf,
+              lane);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    });
   }
 
   tc_fence_before();
@@ -543,26 +588,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
     const int half = ew >> 2;      // which 32-column chunks (every EPI_WARPS/4-th) it owns
     float* buf = epi_buf + ew * 32 * GEMM_EPI_STRIDE;
     const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int tile = pair; tile < tiles; tile += npairs) {
-      int mt, nt;
-      tile_mn(tile, num_m, num_n, args.group_m, mt, nt);
-      const int m0 = mt * 2 * GEMM_BM + rank * GEMM_BM;
-      const int n0 = nt * BN;
-      const int row0 = m0 + q * 32;
-      const int rows = min(32, args.M - row0);
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      if (rows > 0)
-        epi_tile<BN, EPI, C::EPI_WARPS / 4>(args, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN,
-                                            row0, rows, n0, half, buf, lane);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
-    }
+    epi_dispatch(args, [&](auto fmt_c, auto r16_c) {
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = pair; tile < tiles; tile += npairs) {
+        int mt, nt;
+        tile_mn(tile, num_m, num_n, args.group_m, mt, nt);
+        const int m0 = mt * 2 * GEMM_BM + rank * GEMM_BM;
+        const int n0 = nt * BN;
+        const int row0 = m0 + q * 32;
+        const int rows = min(32, args.M - row0);
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        if (rows > 0)
+          epi_tile_t<BN, EPI, C::EPI_WARPS / 4, decltype(fmt_c)::value, decltype(r16_c)::value>(
+              args, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, row0, rows, n0, half, buf,
+              lane);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    });
   }
 
   tc_fence_before();

@@ -334,20 +334,25 @@ __device__ __forceinline__ float load16(const uint16_t* p, size_t i, int fmt) {
                         : __bfloat162float(__ushort_as_bfloat16(p[i]));
 }
 
+// 1/x via MUFU.RCP (approximate, flushes denormals)
+__device__ __forceinline__ float fast_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 // gelu_tanh(x) = 0.5 x (1 + tanh(z)), z = sqrt(2/pi) (x + 0.044715 x^3)
 // (`encoder.py:47-49`), evaluated as the algebraically identical x / (1 + e^{-2z})
-// on a pair with packed fp32 math: MUFU.EX2 and a fast division instead of
-// tanhf's ~25-instruction path, no cancellation for negative x, relative error a
-// few fp32 ulp; e^{-2z} is clamped so the division never sees an infinite
-// denominator.
+// on a pair with packed fp32 math: two MUFU ops (EX2, RCP) instead of tanhf's
+// ~25-instruction path, no cancellation for negative x, relative error a few
+// fp32 ulp.
 __device__ __forceinline__ float2 gelu_tanh2(float2 x) {
   const float c2 = -2.0f * 0.7978845608028654f * 1.4426950408889634f;
-  const float2 x2 = fmul2(x, x);
-  const float2 x3 = fmul2(x2, x);
-  const float2 z = fmul2(make_float2(c2, c2), ffma2(make_float2(0.044715f, 0.044715f), x3, x));
-  const float e0 = fminf(fast_exp2(z.x), 1e30f), e1 = fminf(fast_exp2(z.y), 1e30f);
-  const float2 den = fadd2(make_float2(1.0f, 1.0f), make_float2(e0, e1));
-  return make_float2(__fdividef(x.x, den.x), __fdividef(x.y, den.y));
+  // z = c2 (x + 0.044715 x^3) = x (c2 + c2 0.044715 x^2)
+  const float2 z = fmul2(x, ffma2(make_float2(c2 * 0.044715f, c2 * 0.044715f), fmul2(x, x),
+                                  make_float2(c2, c2)));
+  const float2 den = fadd2(make_float2(1.0f, 1.0f), make_float2(fast_exp2(z.x), fast_exp2(z.y)));
+  // e^{-2z} = inf (x << 0): 1/inf = 0 -> gelu = -0, the correctly signed limit
+  return fmul2(x, make_float2(fast_rcp(den.x), fast_rcp(den.y)));
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
