@@ -66,61 +66,79 @@ __device__ __forceinline__ void ln_load_row(const void* __restrict__ yv, int t, 
   }
 }
 
-template <int V4, bool IN16>
+// R16 (reference fp16 mode): the output is rounded to binary16, so the hi piece is
+// that rounding and the lo piece is exactly 0.
+template <int V4, bool IN16, bool R16>
 __global__ void __launch_bounds__(256)
     layernorm_kernel(const void* __restrict__ yv, int T, int d, int ld,
                      const float* __restrict__ g, const float* __restrict__ bta,
                      float* __restrict__ out32, uint16_t* __restrict__ oh,
-                     uint16_t* __restrict__ ol, int fmt, int r16, int* ovf) {
+                     uint16_t* __restrict__ ol, int fmt, int* ovf) {
   const int lane = threadIdx.x & 31;
   const int n4 = d >> 2;
-  bool ok = true;
-  {
-    const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (t >= T) return;
-    float4 v[V4];
-    ln_load_row<V4, IN16>(yv, t, ld, n4, lane, v);
-    float s = 0.f;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  float4 v[V4];
+  ln_load_row<V4, IN16>(yv, t, ld, n4, lane, v);
+  float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int i = 0; i < V4; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-    const float mean = warp_sum(s) / (float)d;
-    float q = 0.f;
+  for (int i = 0; i < V4; ++i)
+    s2 = fadd2(s2, fadd2(make_float2(v[i].x, v[i].y), make_float2(v[i].z, v[i].w)));
+  const float mean = warp_sum(s2.x + s2.y) / (float)d;
+  const float2 nm = make_float2(-mean, -mean);
+  float2 q2 = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int i = 0; i < V4; ++i) {
-      if (i * 32 + lane < n4) {
-        const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, e = v[i].w - mean;
-        q += (a * a + b * b) + (c * c + e * e);
-      }
+  for (int i = 0; i < V4; ++i) {
+    if (i * 32 + lane < n4) {
+      const float2 a = fadd2(make_float2(v[i].x, v[i].y), nm);
+      const float2 c = fadd2(make_float2(v[i].z, v[i].w), nm);
+      q2 = ffma2(a, a, q2);
+      q2 = ffma2(c, c, q2);
     }
-    const float rstd = 1.0f / sqrtf(warp_sum(q) / (float)d + 1e-5f);
-    const size_t o = (size_t)t * ld;
+  }
+  const float rstd = 1.0f / sqrtf(warp_sum(q2.x + q2.y) / (float)d + 1e-5f);
+  const float2 rs2 = make_float2(rstd, rstd);
+  const size_t o = (size_t)t * ld;
+  float amax = 0.f;
+  uint32_t hinf = 0;
 #pragma unroll
-    for (int i = 0; i < V4; ++i) {
-      const int c = i * 32 + lane;
-      if (c < n4) {
-        const float4 gg = reinterpret_cast<const float4*>(g)[c];
-        const float4 bb = reinterpret_cast<const float4*>(bta)[c];
-        float r[4] = {(v[i].x - mean) * rstd * gg.x + bb.x, (v[i].y - mean) * rstd * gg.y + bb.y,
-                      (v[i].z - mean) * rstd * gg.z + bb.z, (v[i].w - mean) * rstd * gg.w + bb.w};
-        if (r16) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) r[j] = __half2float(__float2half_rn(r[j]));
+  for (int i = 0; i < V4; ++i) {
+    const int c = i * 32 + lane;
+    if (c < n4) {
+      const float4 gg = reinterpret_cast<const float4*>(g)[c];
+      const float4 bb = reinterpret_cast<const float4*>(bta)[c];
+      const float2 r01 = ffma2(fmul2(fadd2(make_float2(v[i].x, v[i].y), nm), rs2),
+                               make_float2(gg.x, gg.y), make_float2(bb.x, bb.y));
+      const float2 r23 = ffma2(fmul2(fadd2(make_float2(v[i].z, v[i].w), nm), rs2),
+                               make_float2(gg.z, gg.w), make_float2(bb.z, bb.w));
+      if (R16) {
+        const __half2 h01 = __floats2half2_rn(r01.x, r01.y), h23 = __floats2half2_rn(r23.x, r23.y);
+        const uint32_t u01 = *reinterpret_cast<const uint32_t*>(&h01);
+        const uint32_t u23 = *reinterpret_cast<const uint32_t*>(&h23);
+        // |h| >= 0x7c00 (inf) sets bit 15 of its half after + 0x0400 (no carry out)
+        hinf |= ((u01 & 0x7fff7fffu) + 0x04000400u) | ((u23 & 0x7fff7fffu) + 0x04000400u);
+        if (out32) {
+          const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+          reinterpret_cast<float4*>(out32 + o)[c] = make_float4(f01.x, f01.y, f23.x, f23.y);
         }
-        if (out32) reinterpret_cast<float4*>(out32 + o)[c] = make_float4(r[0], r[1], r[2], r[3]);
+        if (oh) reinterpret_cast<uint2*>(oh + o)[c] = make_uint2(u01, u23);
+        if (ol) reinterpret_cast<uint2*>(ol + o)[c] = make_uint2(0u, 0u);
+      } else {
+        if (out32) reinterpret_cast<float4*>(out32 + o)[c] = make_float4(r01.x, r01.y, r23.x, r23.y);
         if (oh) {
-          // fp16 range: |r| >= 65520 rounds to inf -> flag (one test per 4 values)
-          if (fmt == FMT_F16)
-            ok &= !(fmaxf(fmaxf(fabsf(r[0]), fabsf(r[1])), fmaxf(fabsf(r[2]), fabsf(r[3]))) >= 65520.f);
+          // fp16 range: |r| >= 65520 rounds to inf -> flag
+          amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r01.x), fabsf(r01.y)), fmaxf(fabsf(r23.x), fabsf(r23.y))));
           uint32_t h01, h23, l01, l23;
-          split2(r[0], r[1], fmt, h01, l01);
-          split2(r[2], r[3], fmt, h23, l23);
+          split2(r01.x, r01.y, fmt, h01, l01);
+          split2(r23.x, r23.y, fmt, h23, l23);
           reinterpret_cast<uint2*>(oh + o)[c] = make_uint2(h01, h23);
           if (ol) reinterpret_cast<uint2*>(ol + o)[c] = make_uint2(l01, l23);
         }
       }
     }
   }
-  if (!ok && ovf) atomicOr(ovf, 1);
+  const bool bad = R16 ? (hinf & 0x80008000u) != 0 : (fmt == FMT_F16 && amax >= 65520.f);
+  if (bad && oh && ovf) atomicOr(ovf, 1);
 }
 
 // Scalar fallback for d % 4 != 0.
@@ -510,8 +528,12 @@ static cudaError_t ln_launch(const void* y, int T, int d, int ld, const float* g
                              float* out32, uint16_t* oh, uint16_t* ol, int fmt, int r16, int* ovf,
                              int rows_blocks, cudaStream_t st) {
   // 4 rows (warps) per CTA: small CTAs retire as soon as their rows are done
-  layernorm_kernel<V4, IN16><<<(T + 3) / 4, 128, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol, fmt,
-                                                          r16, ovf);
+  if (r16)
+    layernorm_kernel<V4, IN16, true><<<(T + 3) / 4, 128, 0, st>>>(y, T, d, ld, g, b, out32, oh, ol,
+                                                                  fmt, ovf);
+  else
+    layernorm_kernel<V4, IN16, false><<<(T + 3) / 4, 128, 0, st>>>(y, T, d, ld, g, b, out32, oh,
+                                                                   ol, fmt, ovf);
   return cudaGetLastError();
 }
 

@@ -137,6 +137,7 @@ struct Uploader {
 struct mfg_ctx {
   int device = 0, precision = MFG_PREC_FP32, num_sms = 148;
   bool split = true, pre_norm = false, profile = false;
+  bool res_bf16 = false;   // bf16 mode: residual stream as bf16 hi/lo pieces (post-norm)
   bool r16 = false;        // reference binary16 mode: every tensor and activation is fp16
   int fmt = FMT_F16;       // 16-bit operand format of every GEMM operand
   int* d_ovf = nullptr;    // fp16 range overflow flag (set by any producer)
@@ -238,14 +239,14 @@ struct mfg_ctx {
   }
 
   // ---------------------------------------------------------------- setup
-  void make_act(Act& a, int64_t rows, int cols_pad) {
+  void make_act(Act& a, int64_t rows, int cols_pad, bool with_lo) {
     char err[256];
     a.rows = pad128(rows);
     a.ld = cols_pad;
     a.hi = dalloc<uint16_t>((size_t)a.rows * a.ld);
     if (!make_tmap_u16(&a.mh, a.hi, a.rows, a.ld, a.ld, GEMM_BM, err, sizeof err))
       throw Fail{MFG_ERR_RUNTIME, err};
-    if (split) {
+    if (with_lo) {
       a.lo = dalloc<uint16_t>((size_t)a.rows * a.ld);
       if (!make_tmap_u16(&a.ml, a.lo, a.rows, a.ld, a.ld, GEMM_BM, err, sizeof err))
         throw Fail{MFG_ERR_RUNTIME, err};
@@ -458,7 +459,7 @@ struct mfg_ctx {
     cap_records = cfg.max_records > 0 ? cfg.max_records : 4096;
     x32 = dalloc<float>((size_t)cap_tokens * dp);
     y32 = dalloc<float>((size_t)cap_tokens * dp);
-    make_act(qa, cap_tokens, qkv_ld);
+    make_act(qa, cap_tokens, qkv_ld, split);
     {
       char err[256];
       if (!make_tmap_u16(&qm32h, qa.hi, qa.rows, qa.ld, qa.ld, 32, err, sizeof err))
@@ -472,21 +473,24 @@ struct mfg_ctx {
         throw Fail{MFG_ERR_RUNTIME, err};
     }
     att_tc = (d / H == 64 || d / H == 80) && (d % 64 == 0);
-    make_act(xa, cap_tokens, dp);
-    make_act(ca, cap_tokens, dp);
-    make_act(ha, cap_tokens, fp);
-    make_act(fa, cap_records, Fp);
+    // post-norm bf16 mode: the residual stream travels as bf16 hi/lo pieces of
+    // the layer input (~16 significant bits instead of a separate fp32 copy)
+    res_bf16 = !split && !r16 && !pre_norm;
+    make_act(xa, cap_tokens, dp, split || res_bf16);
+    make_act(ca, cap_tokens, dp, split);
+    make_act(ha, cap_tokens, fp, split);
+    make_act(fa, cap_records, Fp, split);
     {
       const int64_t ns = (int64_t)cap_records * n_roles;
-      make_act(cb, ns, dp);
-      make_act(xb, ns, dp);
-      make_act(hb, ns, fp);
-      make_act(qb, ns, dp);
+      make_act(cb, ns, dp, split);
+      make_act(xb, ns, dp, split || res_bf16);
+      make_act(hb, ns, fp, split);
+      make_act(qb, ns, dp, split);
       x32b = dalloc<float>((size_t)pad128(ns) * dp);
       y32b = dalloc<float>((size_t)pad128(ns) * dp);
     }
     ga.resize(head.size() - 1);
-    for (size_t j = 0; j + 1 < head.size(); ++j) make_act(ga[j], cap_records, head[j].Npad);
+    for (size_t j = 0; j + 1 < head.size(); ++j) make_act(ga[j], cap_records, head[j].Npad, split);
     hout = dalloc<float>((size_t)pad128(cap_records) * head.back().Npad);
     dscores = dalloc<float>(cap_records);
     d_ids = dalloc<int32_t>(cap_tokens);
@@ -564,17 +568,18 @@ struct mfg_ctx {
     const int Ti = (int)T;
     {
       int e = ev_begin();
-      // post-norm with split (or exact binary16) operands: the residual stream
-      // lives only in the operand pieces xa (hi + lo ~ 22 bits), so LayerNorm
+      // post-norm: the residual stream lives only in the operand pieces xa (fp16
+      // hi + lo ~ 22 bits; exact binary16 in fp16 mode; bf16 hi + lo ~ 16 bits in
+      // bf16 mode), so LayerNorm
       // writes 8 instead of 12 bytes per element; x32 is written once, by the
       // last LayerNorm, for pooling
-      const bool res16 = !pre_norm && (split || r16) && !layers.empty();
+      const bool res16 = !pre_norm && (split || r16 || res_bf16) && !layers.empty();
       CK(launch_embed(d_ids, d_cu, nseq, (int)man.vocab_size, d, tok, pos, res16 ? nullptr : x32,
                       dp, pre_norm ? nullptr : xa.hi, pre_norm ? nullptr : xa.lo, fmt, r16, d_ovf,
                       st));
       ev_end(e, C_EMB, 0, (double)T * d * (8 + (res16 ? 0 : 4) + (pre_norm ? 0 : (split ? 4 : 2))));
     }
-    const bool res16 = !pre_norm && (split || r16) && !layers.empty();
+    const bool res16 = !pre_norm && (split || r16 || res_bf16) && !layers.empty();
     const bool y16 = res16 && r16;  // O-proj / FFN2 outputs as binary16 (reference fp16 mode)
     const int S = nseq;
     // BOS rows of xa (the layer input pieces) and, when the residual is fp32, of x32
