@@ -44,65 +44,231 @@ inline uint64_t mix(uint64_t x) {
 
 struct mfh_vocab {
   int32_t size = 0, max_piece = 0;
-  // trie: edge table keyed by (node << 21 | code point), open addressing
-  std::vector<uint64_t> keys;
-  std::vector<int32_t> vals;
+  // Trie: edge table keyed by (node << 21 | code point), open addressing. One
+  // 16-byte slot holds the key, the child node and the token id ending at the
+  // child, so each step of a walk touches one cache line.
+  struct Edge {
+    uint64_t key;
+    int32_t child, term;
+  };
+  std::vector<Edge> edges;
   uint64_t mask = 0;
-  std::vector<int32_t> term;  // token id ending at node, -1 if none
-
-  int32_t child(int32_t node, uint32_t cp) const {
+  int32_t n_nodes = 1;
+  int32_t child(int32_t node, uint32_t cp, int32_t& term) const {
     const uint64_t k = ((uint64_t)node << 21) | cp;
     for (uint64_t h = mix(k) & mask;; h = (h + 1) & mask) {
-      if (keys[h] == k) return vals[h];
-      if (keys[h] == ~0ull) return -1;
+      const Edge& e = edges[h];
+      if (e.key == k) {
+        term = e.term;
+        return e.child;
+      }
+      if (e.key == ~0ull) return -1;
     }
   }
-  void insert_edge(uint64_t k, int32_t v) {
-    for (uint64_t h = mix(k) & mask;; h = (h + 1) & mask) {
-      if (keys[h] == ~0ull) {
-        keys[h] = k;
-        vals[h] = v;
-        return;
+  Edge& edge_slot(uint64_t k) {
+    for (uint64_t h = mix(k) & mask;; h = (h + 1) & mask)
+      if (edges[h].key == k || edges[h].key == ~0ull) return edges[h];
+  }
+
+  // Whole-piece table keyed by the piece's UTF-8 bytes (text and vocabulary both
+  // come from Python's canonical encoder, so byte equality is code-point
+  // equality). When no piece holds the word marker after its first code point,
+  // no match can run past the end of a word, so the piece equal to the rest of
+  // the word (if any) is the longest match there: one lookup instead of a walk
+  // per code point. Pieces of <= 16 bytes compare inside their 32-byte slot.
+  struct Piece {
+    uint64_t h;
+    int32_t id, len;
+    unsigned char b[16];
+  };
+  std::vector<Piece> pieces;
+  std::vector<std::string> long_pieces;  // > 16 bytes, indexed by slot
+  std::vector<int32_t> long_of;          // slot -> index into long_pieces (-1)
+  uint64_t pmask = 0;
+  int32_t max_piece_bytes = 0;
+  bool words_closed = true;  // no piece has the marker at index > 0
+
+  static uint64_t hash_bytes(const unsigned char* p, size_t n) {
+    uint64_t h = 0x243F6A8885A308D3ull ^ n;
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+      uint64_t w;
+      std::memcpy(&w, p + i, 8);
+      h = mix(h ^ w);
+    }
+    uint64_t w = 0;
+    std::memcpy(&w, p + i, n - i);
+    return mix(h ^ w);
+  }
+
+  // id of the piece whose bytes are p[0..n), -1 if none
+  int32_t whole(const unsigned char* p, size_t n) const {
+    if (n == 0 || (int64_t)n > max_piece_bytes) return -1;
+    return whole_h(p, n, hash_bytes(p, n));
+  }
+  int32_t whole_h(const unsigned char* p, size_t n, uint64_t hv) const {
+    for (uint64_t h = hv & pmask;; h = (h + 1) & pmask) {
+      const Piece& q = pieces[h];
+      if (q.id < 0) return -1;
+      if (q.h == hv && q.len == (int32_t)n) {
+        const unsigned char* r = n <= 16 ? q.b : (const unsigned char*)long_pieces[long_of[h]].data();
+        if (std::memcmp(r, p, n) == 0) return q.id;
       }
     }
+  }
+  void add_piece(const unsigned char* p, size_t n, int32_t id) {
+    const uint64_t hv = hash_bytes(p, n);
+    for (uint64_t h = hv & pmask;; h = (h + 1) & pmask) {
+      Piece& q = pieces[h];
+      if (q.id < 0) {
+        q.h = hv;
+        q.id = id;
+        q.len = (int32_t)n;
+        if (n <= 16) {
+          std::memcpy(q.b, p, n);
+        } else {
+          long_of[h] = (int32_t)long_pieces.size();
+          long_pieces.emplace_back((const char*)p, n);
+        }
+        max_piece_bytes = std::max(max_piece_bytes, (int32_t)n);
+        return;
+      }
+      if (whole(p, n) >= 0) return;  // first occurrence wins
+    }
+  }
+
+  // greedy longest match of s[pos..end) from the trie; returns the match length
+  // (0: no piece matches) and its id
+  size_t walk(const uint32_t* s, size_t pos, size_t end, int32_t& id) const {
+    int32_t node = 0;
+    size_t best_len = 0;
+    id = -1;
+    for (size_t j = pos; j < end; ++j) {
+      int32_t term;
+      node = child(node, s[j], term);
+      if (node < 0) break;
+      if (term >= 0) {
+        id = term;
+        best_len = j - pos + 1;
+      }
+    }
+    return best_len;
   }
 
   // Vocabulary.encode: whitespace split, "▁"-join, greedy longest match.
   void encode(const char* text, int64_t nbytes, std::vector<uint32_t>& s,
               std::vector<int32_t>& out) const {
-    s.clear();
-    const unsigned char* p = (const unsigned char*)text;
-    const unsigned char* e = p + nbytes;
-    bool in_word = false;
-    while (p < e) {
-      const uint32_t c = next_cp(p, e);
-      if (py_isspace(c)) {
-        in_word = false;
-      } else {
-        if (!in_word) s.push_back(MARKER);
-        in_word = true;
-        s.push_back(c);
-      }
-    }
-    const size_t n = s.size();
-    size_t pos = 0;
-    while (pos < n) {
-      int32_t node = 0, best = -1;
-      size_t best_len = 0;
-      for (size_t j = pos; j < n; ++j) {
-        node = child(node, s[j]);
-        if (node < 0) break;
-        if (term[node] >= 0) {
-          best = term[node];
-          best_len = j - pos + 1;
+    const unsigned char* p0 = (const unsigned char*)text;
+    const unsigned char* e = p0 + nbytes;
+    if (!words_closed) {  // pieces may span words: walk the whole "▁"-joined sequence
+      s.clear();
+      bool in_word = false;
+      for (const unsigned char* p = p0; p < e;) {
+        const uint32_t c = next_cp(p, e);
+        if (py_isspace(c)) {
+          in_word = false;
+        } else {
+          if (!in_word) s.push_back(MARKER);
+          in_word = true;
+          s.push_back(c);
         }
       }
-      if (best < 0) {
-        out.push_back(UNK);
-        pos += 1;
-      } else {
-        out.push_back(best);
-        pos += best_len;
+      const size_t n = s.size();
+      size_t pos = 0;
+      while (pos < n) {
+        int32_t id;
+        const size_t len = walk(s.data(), pos, n, id);
+        out.push_back(len ? id : UNK);
+        pos += len ? len : 1;
+      }
+      return;
+    }
+    // Words are cut, hashed and their table slots prefetched in batches of 32,
+    // then resolved in order: the independent lookups overlap their cache misses.
+    constexpr int BATCH = 32;
+    struct Word {
+      const unsigned char* w0;
+      uint32_t wb;
+      uint64_t h;  // hash of "▁" + word
+      bool fits;   // short enough to be one piece
+    };
+    Word batch[BATCH];
+    unsigned char key[3 + 64];
+    key[0] = 0xE2, key[1] = 0x96, key[2] = 0x81;  // "▁" in UTF-8
+    std::vector<uint32_t> boff;                      // byte offset of each code point
+    const unsigned char* p = p0;
+    bool more = true;
+    while (more) {
+      int nb = 0;
+      while (nb < BATCH) {
+        // next word: [w0, w1) bytes of non-space code points
+        const unsigned char* w0 = nullptr;
+        while (p < e) {
+          const unsigned char* q = p;
+          const uint32_t c = *p < 0x80 ? *p++ : next_cp(p, e);
+          if (!py_isspace(c)) {
+            w0 = q;
+            break;
+          }
+        }
+        if (!w0) {
+          more = false;
+          break;
+        }
+        while (p < e) {
+          const unsigned char* q = p;
+          const uint32_t c = *p < 0x80 ? *p++ : next_cp(p, e);
+          if (py_isspace(c)) {
+            p = q;
+            break;
+          }
+        }
+        Word& w = batch[nb++];
+        w.w0 = w0;
+        w.wb = (uint32_t)(p - w0);
+        w.fits = w.wb + 3 <= (uint32_t)max_piece_bytes && w.wb <= 64;
+        if (w.fits) {
+          std::memcpy(key + 3, w0, w.wb);
+          w.h = hash_bytes(key, w.wb + 3);
+          __builtin_prefetch(&pieces[w.h & pmask]);
+        }
+      }
+      for (int i = 0; i < nb; ++i) {
+        const Word& w = batch[i];
+        if (w.fits) {  // whole word, marker included
+          std::memcpy(key + 3, w.w0, w.wb);
+          const int32_t id = whole_h(key, w.wb + 3, w.h);
+          if (id >= 0) {
+            out.push_back(id);
+            continue;
+          }
+        }
+        // the word is not one piece: greedy walk over its code points
+        const unsigned char* w0 = w.w0;
+        const unsigned char* w1 = w0 + w.wb;
+        s.clear();
+        boff.clear();
+        s.push_back(MARKER);
+        boff.push_back(0);
+        for (const unsigned char* q = w0; q < w1;) {
+          boff.push_back((uint32_t)(q - w0));
+          s.push_back(next_cp(q, w1));
+        }
+        const size_t n = s.size();
+        size_t pos = 0;
+        while (pos < n) {
+          if (pos > 0) {  // the rest of the word as one piece?
+            const int32_t id = whole(w0 + boff[pos], w.wb - boff[pos]);
+            if (id >= 0) {
+              out.push_back(id);
+              break;
+            }
+          }
+          int32_t wid;
+          const size_t len = walk(s.data(), pos, n, wid);
+          out.push_back(len ? wid : UNK);
+          pos += len ? len : 1;
+        }
       }
     }
   }
@@ -130,27 +296,37 @@ extern "C" int mfh_vocab_create(const char* blob, int64_t nbytes, int32_t n_toke
   for (int32_t i = N_SPECIAL; i < n_tokens; ++i) cps += toks[i].second - toks[i].first;
   uint64_t cap = 16;
   while (cap < (uint64_t)(2 * cps + 16)) cap <<= 1;
-  v->keys.assign(cap, ~0ull);
-  v->vals.assign(cap, -1);
+  v->edges.assign(cap, mfh_vocab::Edge{~0ull, -1, -1});
   v->mask = cap - 1;
-  v->term.assign(1, -1);
+  uint64_t pcap = 16;
+  while (pcap < (uint64_t)(2 * n_tokens + 16)) pcap <<= 1;
+  v->pieces.assign(pcap, mfh_vocab::Piece{0, -1, 0, {}});
+  v->long_of.assign(pcap, -1);
+  v->pmask = pcap - 1;
+  std::vector<uint32_t> cp;
   for (int32_t i = N_SPECIAL; i < n_tokens; ++i) {
     const unsigned char* p = (const unsigned char*)blob + toks[i].first;
     const unsigned char* e = (const unsigned char*)blob + toks[i].second;
-    int32_t node = 0, len = 0;
+    cp.clear();
+    int32_t node = 0;
+    mfh_vocab::Edge* last = nullptr;
     while (p < e) {
       const uint32_t c = next_cp(p, e);
-      int32_t ch = v->child(node, c);
-      if (ch < 0) {
-        ch = (int32_t)v->term.size();
-        v->term.push_back(-1);
-        v->insert_edge(((uint64_t)node << 21) | c, ch);
+      if (c == MARKER && !cp.empty()) v->words_closed = false;
+      cp.push_back(c);
+      mfh_vocab::Edge& ed = v->edge_slot(((uint64_t)node << 21) | c);
+      if (ed.key == ~0ull) {
+        ed.key = ((uint64_t)node << 21) | c;
+        ed.child = v->n_nodes++;
       }
-      node = ch;
-      ++len;
+      node = ed.child;
+      last = &ed;
     }
-    if (node != 0 && v->term[node] < 0) v->term[node] = i;  // first occurrence wins
-    v->max_piece = std::max(v->max_piece, len);
+    if (last && last->term < 0) last->term = i;  // first occurrence wins
+    if (!cp.empty())
+      v->add_piece((const unsigned char*)blob + toks[i].first,
+                   (size_t)(toks[i].second - toks[i].first), i);
+    v->max_piece = std::max(v->max_piece, (int32_t)cp.size());
   }
   *out = v;
   return 0;

@@ -91,6 +91,33 @@ def test_matches_brute_force_segmenter(data):
     assert v.encode(text) == _brute(stream, tokens) == otk.OracleVocab(fx.SPECIALS + pieces).encode(text)
 
 
+@st.composite
+def closed_vocab_and_text(draw):
+    """Pieces with the marker only in front (the C++ whole-word fast path), long
+    pieces (> 16 UTF-8 bytes) included, words that are / are not whole pieces."""
+    body = st.text(alphabet="abcdé北", min_size=1, max_size=7)
+    pieces = draw(st.lists(st.tuples(st.booleans(), body).map(lambda t: (MARK if t[0] else "") + t[1]),
+                           min_size=1, max_size=14, unique=True))
+    pieces = [p for p in pieces if p not in fx.SPECIALS]
+    words = draw(st.lists(st.one_of(st.sampled_from([p.lstrip(MARK) for p in pieces] or ["a"]),
+                                    st.text(alphabet="abcdé北", min_size=1, max_size=9)),
+                          max_size=8))
+    return pieces, " ".join(words)
+
+
+@settings(max_examples=300, deadline=None)
+@given(data=closed_vocab_and_text())
+def test_whole_word_fast_path_matches_brute_force(data):
+    pieces, text = data
+    if not pieces:
+        return
+    v = mf.Vocabulary(fx.SPECIALS + pieces)
+    words = text.split()
+    stream = MARK + MARK.join(words) if words else ""
+    tokens = {p: i + 5 for i, p in enumerate(pieces)}
+    assert v.encode(text) == _brute(stream, tokens)
+
+
 def test_python_whitespace_set_exactly():
     v = mf.Vocabulary(fx.SPECIALS + [MARK + "a", MARK + "b"])
     a, b = 5, 6
