@@ -42,6 +42,20 @@ int64_t mfh_encode_records(const mfh_vocab* v, int32_t kind, int32_t n, const ch
                            const int64_t* field_off, int32_t max_len, int32_t n_threads,
                            int32_t* ids_out, int64_t ids_cap, int64_t* seq_off);
 
+/* Native TSV intake + encode_fields (replaces the per-record
+ * Python loop `records_from_tsv_lines` -> `EvalRecord.field_values` ->
+ * `encode_fields`, pkg/src/metricforge/evaluate.py:112-123, 179-196 and
+ * vocab.py:104-143). blob holds n_lines lines back to back, line i =
+ * blob[line_off[i] .. line_off[i+1]); each is rstrip("\n")-ed and split on
+ * '\t'. Output as mfh_encode_records. Returns 0; 3 when a line has the wrong
+ * column count (*bad_line = its index within this call, *bad_cols = its count;
+ * checked for all lines before any max_len error); 2 on bad arguments or a
+ * max_len too small for the specials; -(needed) if ids_cap is too small. */
+int64_t mfh_encode_tsv(const mfh_vocab* v, int32_t kind, const char* blob,
+                       const int64_t* line_off, int64_t n_lines, int32_t max_len,
+                       int32_t n_threads, int32_t* ids_out, int64_t ids_cap, int64_t* seq_off,
+                       int64_t* bad_line, int32_t* bad_cols);
+
 /* order[pos] = original index; windows of mini_batch*factor, stable sort by
  * (-length, index) inside a window when sort != 0. */
 int mfh_plan(const int64_t* lengths, int64_t n, int32_t mini_batch, int32_t factor, int32_t sort,

@@ -355,13 +355,14 @@ struct Part {
 };
 
 // encode_fields for records [r0, r1) (vocab.py:104-143)
-void encode_range(const mfh_vocab* v, int kind, int r0, int r1, const char* blob,
-                  const int64_t* off, int max_len, Part& out) {
+// Field k of record r is blob[span[2(r nf + k)] .. span[2(r nf + k) + 1]).
+void encode_range(const mfh_vocab* v, int kind, int64_t r0, int64_t r1, const char* blob,
+                  const int64_t* span, int max_len, Part& out) {
   const int nf = kind == 1 ? 3 : 2;
   std::vector<uint32_t> s;
   std::vector<int32_t> a, b;
-  for (int r = r0; r < r1; ++r) {
-    const int64_t* fo = off + (int64_t)r * nf;
+  for (int64_t r = r0; r < r1; ++r) {
+    const int64_t* fs = span + 2 * r * nf;
     if (kind == 2) {
       if (max_len < 3) {
         out.err = 2;
@@ -369,8 +370,8 @@ void encode_range(const mfh_vocab* v, int kind, int r0, int r1, const char* blob
       }
       a.clear();
       b.clear();
-      v->encode(blob + fo[0], fo[1] - fo[0], s, a);
-      v->encode(blob + fo[1], fo[2] - fo[1], s, b);
+      v->encode(blob + fs[0], fs[1] - fs[0], s, a);
+      v->encode(blob + fs[2], fs[3] - fs[2], s, b);
       // pop from the longer side, ties pop the second (closed form)
       const int64_t budget = max_len - 3;
       int64_t na = (int64_t)a.size(), nb = (int64_t)b.size();
@@ -388,7 +389,7 @@ void encode_range(const mfh_vocab* v, int kind, int r0, int r1, const char* blob
     } else {
       for (int k = 0; k < nf; ++k) {
         a.clear();
-        v->encode(blob + fo[k], fo[k + 1] - fo[k], s, a);
+        v->encode(blob + fs[2 * k], fs[2 * k + 1] - fs[2 * k], s, a);
         int64_t n = (int64_t)a.size() + 2;
         if (n > max_len) {
           if (max_len < 2) {
@@ -411,28 +412,20 @@ void encode_range(const mfh_vocab* v, int kind, int r0, int r1, const char* blob
   }
 }
 
-}  // namespace
-
-extern "C" int64_t mfh_encode_records(const mfh_vocab* v, int32_t kind, int32_t n,
-                                      const char* blob, const int64_t* field_off,
-                                      int32_t max_len, int32_t n_threads, int32_t* ids_out,
-                                      int64_t ids_cap, int64_t* seq_off) {
-  if (!v || kind < 0 || kind > 2 || n < 0) return 2;
-  if (n == 0) {
-    seq_off[0] = 0;
-    return 0;
-  }
+// Runs encode_range over n records on th threads and concatenates the parts.
+int64_t encode_spans(const mfh_vocab* v, int kind, int64_t n, const char* blob,
+                     const int64_t* span, int max_len, int n_threads, int32_t* ids_out,
+                     int64_t ids_cap, int64_t* seq_off) {
   int th = n_threads > 0 ? n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
-  th = std::max(1, std::min(th, (n + 63) / 64));
+  th = (int)std::max<int64_t>(1, std::min<int64_t>(th, (n + 63) / 64));
   std::vector<Part> parts(th);
   std::vector<std::thread> pool;
   for (int t = 0; t < th; ++t) {
-    const int r0 = (int)((int64_t)n * t / th), r1 = (int)((int64_t)n * (t + 1) / th);
+    const int64_t r0 = n * t / th, r1 = n * (t + 1) / th;
     if (th == 1)
-      encode_range(v, kind, r0, r1, blob, field_off, max_len, parts[t]);
+      encode_range(v, kind, r0, r1, blob, span, max_len, parts[t]);
     else
-      pool.emplace_back(encode_range, v, kind, r0, r1, blob, field_off, max_len,
-                        std::ref(parts[t]));
+      pool.emplace_back(encode_range, v, kind, r0, r1, blob, span, max_len, std::ref(parts[t]));
   }
   for (auto& t : pool) t.join();
   int64_t total = 0;
@@ -452,6 +445,93 @@ extern "C" int64_t mfh_encode_records(const mfh_vocab* v, int32_t kind, int32_t 
     }
   }
   return 0;
+}
+
+}  // namespace
+
+extern "C" int64_t mfh_encode_records(const mfh_vocab* v, int32_t kind, int32_t n,
+                                      const char* blob, const int64_t* field_off,
+                                      int32_t max_len, int32_t n_threads, int32_t* ids_out,
+                                      int64_t ids_cap, int64_t* seq_off) {
+  if (!v || kind < 0 || kind > 2 || n < 0) return 2;
+  if (n == 0) {
+    seq_off[0] = 0;
+    return 0;
+  }
+  const int nf = kind == 1 ? 3 : 2;
+  std::vector<int64_t> span(2 * (size_t)n * nf);
+  for (int64_t j = 0; j < (int64_t)n * nf; ++j) {
+    span[2 * j] = field_off[j];
+    span[2 * j + 1] = field_off[j + 1];
+  }
+  return encode_spans(v, kind, n, blob, span.data(), max_len, n_threads, ids_out, ids_cap,
+                      seq_off);
+}
+
+// Native TSV intake (`evaluate.py:117-123`: line.rstrip("\n").split("\t"), exact
+// column count else ColumnCountError(line index)): column check over all lines
+// first (a bad line wins over a max_len error, as in the reference's order),
+// then encode_fields on the field spans.
+extern "C" int64_t mfh_encode_tsv(const mfh_vocab* v, int32_t kind, const char* blob,
+                                  const int64_t* line_off, int64_t n_lines, int32_t max_len,
+                                  int32_t n_threads, int32_t* ids_out, int64_t ids_cap,
+                                  int64_t* seq_off, int64_t* bad_line, int32_t* bad_cols) {
+  if (!v || kind < 0 || kind > 2 || n_lines < 0 || !bad_line || !bad_cols) return 2;
+  *bad_line = -1;
+  *bad_cols = 0;
+  if (n_lines == 0) {
+    seq_off[0] = 0;
+    return 0;
+  }
+  const int nf = kind == 1 ? 3 : 2;
+  std::vector<int64_t> span(2 * (size_t)n_lines * nf);
+  int th = n_threads > 0 ? n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
+  th = (int)std::max<int64_t>(1, std::min<int64_t>(th, (n_lines + 1023) / 1024));
+  std::vector<int64_t> first_bad(th, -1);
+  std::vector<int32_t> first_cols(th, 0);
+  auto split = [&](int t, int64_t l0, int64_t l1) {
+    for (int64_t l = l0; l < l1; ++l) {
+      const int64_t b0 = line_off[l];
+      int64_t b1 = line_off[l + 1];
+      while (b1 > b0 && blob[b1 - 1] == '\n') --b1;  // rstrip("\n")
+      int cols = 0;
+      int64_t st = b0;
+      int64_t* fs = span.data() + 2 * l * nf;
+      for (int64_t i = b0;; ++i) {
+        if (i == b1 || blob[i] == '\t') {
+          if (cols < nf) {
+            fs[2 * cols] = st;
+            fs[2 * cols + 1] = i;
+          }
+          ++cols;
+          st = i + 1;
+          if (i == b1) break;
+        }
+      }
+      if (cols != nf) {
+        first_bad[t] = l;
+        first_cols[t] = cols;
+        return;  // later lines of this chunk cannot be reported first
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < th; ++t) {
+    const int64_t l0 = n_lines * t / th, l1 = n_lines * (t + 1) / th;
+    if (th == 1)
+      split(t, l0, l1);
+    else
+      pool.emplace_back(split, t, l0, l1);
+  }
+  for (auto& t : pool) t.join();
+  for (int t = 0; t < th; ++t)
+    if (first_bad[t] >= 0) {
+      *bad_line = first_bad[t];
+      *bad_cols = first_cols[t];
+      return 3;
+    }
+  return encode_spans(v, kind, n_lines, blob, span.data(), max_len, n_threads, ids_out, ids_cap,
+                      seq_off);
 }
 
 extern "C" int mfh_plan(const int64_t* lengths, int64_t n, int32_t mini_batch, int32_t factor,

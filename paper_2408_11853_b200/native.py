@@ -56,6 +56,9 @@ def host():
             lib.mfh_encode_records.argtypes = [C.c_void_p, i32, i32, C.c_char_p, i64p, i32, i32,
                                                i32p, i64, i64p]
             lib.mfh_encode_records.restype = i64
+            lib.mfh_encode_tsv.argtypes = [C.c_void_p, i32, C.c_char_p, i64p, i64, i32, i32, i32p,
+                                           i64, i64p, i64p, i32p]
+            lib.mfh_encode_tsv.restype = i64
             lib.mfh_plan.argtypes = [i64p, i64, i32, i32, i32, i64p]
             lib.mfh_plan.restype = C.c_int
             lib.mfh_pack_roles.argtypes = [i32p, i64p, i32, i64p, i64, i32p, i64p]

@@ -73,17 +73,22 @@ def shard_plan(seq_off, n_seq, n_records, config: BatchConfig, world: int):
 
 
 def score_sharded(model_score: Callable, vocab, kind, field_texts, max_len, config: BatchConfig,
-                  rank: int, world: int, gather: Optional[Callable] = None, n_threads: int = 0):
+                  rank: int, world: int, gather: Optional[Callable] = None, n_threads: int = 0,
+                  encoded=None):
     """Score `field_texts` (per-record field lists) across `world` ranks.
 
     model_score(ids, cu, n) -> float32[n] scores role-major packed records (e.g.
     GpuScoringModel.score_packed); gather(obj) -> list of obj from all ranks
     (e.g. torch.distributed.all_gather_object). Returns scores in input order
-    (on every rank)."""
+    (on every rank). encoded = ((ids, seq_off), n) skips the tokenisation (records
+    already encoded, e.g. by Vocabulary.encode_tsv)."""
     kind = Kind.parse(kind)
-    n = len(field_texts)
     ns = N_SEQUENCES[kind]
-    ids, seq_off = vocab.encode_batch(kind, field_texts, max_len, n_threads)
+    if encoded is not None:
+        (ids, seq_off), n = encoded
+    else:
+        n = len(field_texts)
+        ids, seq_off = vocab.encode_batch(kind, field_texts, max_len, n_threads)
     order, batches, assign = shard_plan(seq_off, ns, n, config, world)
     mine = assign[rank]
     pos = np.concatenate([np.arange(*batches[b]) for b in mine]) if mine else np.zeros(0, np.int64)
@@ -132,10 +137,20 @@ class DistributedEvaluator:
 
     def evaluate_lines(self, lines) -> ScoreReport:
         kind = self.ev.kind
-        recs = [r.field_values(kind, i) for i, r in enumerate(records_from_tsv_lines(lines, kind))]
-        scores = score_sharded(self.ev.model.score_packed, self.ev.vocab, kind, recs,
+        if isinstance(lines, (list, tuple)) and all(type(l) is str for l in lines):
+            encoded = self.ev.vocab.encode_tsv(kind, lines, self.ev.max_len,
+                                               self.config.tokenizer_threads)
+            n = len(lines)
+        else:
+            recs = [r.field_values(kind, i)
+                    for i, r in enumerate(records_from_tsv_lines(lines, kind))]
+            encoded = self.ev.vocab.encode_batch(kind, recs, self.ev.max_len,
+                                                 self.config.tokenizer_threads)
+            n = len(recs)
+        scores = score_sharded(self.ev.model.score_packed, self.ev.vocab, kind, None,
                                self.ev.max_len, self.config.batch, self.rank, self.world,
-                               self._gather, self.config.tokenizer_threads)
+                               self._gather, self.config.tokenizer_threads,
+                               encoded=(encoded, n))
         return ScoreReport(segment_scores=scores.tolist())
 
     def close(self):

@@ -103,6 +103,52 @@ class Vocabulary:
         return ids[:int(seq_off[-1])], seq_off
 
 
+    def encode_tsv(self, kind: Kind, lines, max_len: int, n_threads: int = 0, first_index: int = 0):
+        """records_from_tsv_lines + field_values + encode_batch for a list of str
+        lines in one native call (`evaluate.py:117-123`). Raises
+        ColumnCountError(first_index + i, ...) for the first bad line. Returns
+        (ids int32[total], seq_off int64[n * n_seqs + 1]) record-major."""
+        from .errors import ColumnCountError
+        from .kinds import FIELDS_REQUIRED
+        kind = Kind.parse(kind)
+        n = len(lines)
+        blob, line_off = lines_blob(lines)
+        ns = N_SEQUENCES[kind]
+        cap = 2 * len(blob) + 4 * ns * n + 8
+        ids = np.empty(cap, dtype=np.int32)
+        seq_off = np.zeros(n * ns + 1, dtype=np.int64)
+        bad_line, bad_cols = C.c_int64(-1), C.c_int32(0)
+        rc = self._lib.mfh_encode_tsv(
+            self._h, KIND_CODE[kind], blob, native.ptr(line_off, C.c_int64), n, int(max_len),
+            int(n_threads), native.ptr(ids, C.c_int32), cap, native.ptr(seq_off, C.c_int64),
+            C.byref(bad_line), C.byref(bad_cols))
+        if rc == 3:
+            raise ColumnCountError(first_index + bad_line.value, len(FIELDS_REQUIRED[kind]),
+                                   bad_cols.value)
+        if rc == 2:
+            need = 3 if kind is Kind.BLEURT else 2
+            what = "BOS, SEP and EOS" if kind is Kind.BLEURT else "BOS and EOS"
+            raise ValueError(f"max_len {max_len} cannot hold {what}" if max_len < need else
+                             "tokenizer failed")
+        if rc != 0:
+            raise RuntimeError(f"mfh_encode_tsv failed ({rc})")
+        return ids[:int(seq_off[-1])], seq_off
+
+
+def lines_blob(lines):
+    """UTF-8 bytes of str lines back to back + their byte offsets [n + 1]."""
+    n = len(lines)
+    off = np.zeros(n + 1, dtype=np.int64)
+    text = "".join(lines)
+    blob = _utf8(text)
+    if len(blob) == len(text):  # ASCII: byte lengths = str lengths
+        np.cumsum(np.fromiter(map(len, lines), dtype=np.int64, count=n), out=off[1:])
+    else:
+        np.cumsum(np.fromiter((len(_utf8(l)) for l in lines), dtype=np.int64, count=n),
+                  out=off[1:])
+    return blob, off
+
+
 def load_vocab(path) -> Vocabulary:
     with open(path, "r", encoding="utf-8") as f:  # universal newlines, like the reference
         text = f.read()

@@ -13,7 +13,7 @@ from oracle import evaluate as oe
 from oracle import fixtures as fx
 from oracle import tokenizer as otk
 from paper_2408_11853_b200.batching import pack_roles, plan_order
-from paper_2408_11853_b200.errors import MissingFieldError, VocabularyError
+from paper_2408_11853_b200.errors import ColumnCountError, MissingFieldError, VocabularyError
 
 MARK = "▁"
 WHITESPACE = [0x9, 0xA, 0xB, 0xC, 0xD, 0x1C, 0x1D, 0x1E, 0x1F, 0x20, 0x85, 0xA0, 0x1680,
@@ -233,4 +233,54 @@ def test_multithreaded_encoding_is_identical():
     fields = [r.field_values(mf.Kind.COMET_QE) for r in recs]
     a = v.encode_batch(mf.Kind.COMET_QE, fields, 40, n_threads=1)
     b = v.encode_batch(mf.Kind.COMET_QE, fields, 40, n_threads=8)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# ---------------------------------------------------------------- native TSV intake
+_FIELD = st.text(alphabet="ab é北\r\x0b" + MARK, max_size=12)
+
+
+@settings(max_examples=200, deadline=None)
+@given(kind=st.sampled_from([mf.Kind.COMET_QE, mf.Kind.COMET, mf.Kind.BLEURT]),
+       rows=st.lists(st.tuples(st.lists(_FIELD, min_size=1, max_size=4),
+                               st.sampled_from(["", "\n", "\n\n", "\r\n"])), max_size=12),
+       max_len=st.sampled_from([3, 5, 64]), threads=st.sampled_from([1, 4]))
+def test_encode_tsv_matches_python_intake(kind, rows, max_len, threads):
+    """mfh_encode_tsv == records_from_tsv_lines -> field_values -> encode_batch,
+    including the ColumnCountError of the first bad line (`evaluate.py:117-123`)."""
+    v = mf.Vocabulary(fx.SPECIALS + [MARK + "a", "b", MARK + "é北", "北", MARK + "ab"])
+    lines = ["\t".join(cols) + end for cols, end in rows]
+    try:
+        recs = list(mf.records_from_tsv_lines(lines, kind))
+        want_err = None
+    except ColumnCountError as e:
+        want_err = (e.line_index, e.expected, e.got)
+    if want_err is not None:
+        with pytest.raises(ColumnCountError) as ei:
+            v.encode_tsv(kind, lines, max_len, threads, first_index=0)
+        assert (ei.value.line_index, ei.value.expected, ei.value.got) == want_err
+        return
+    fields = [r.field_values(kind) for r in recs]
+    want = v.encode_batch(kind, fields, max_len, threads)
+    got = v.encode_tsv(kind, lines, max_len, threads)
+    assert np.array_equal(want[0], got[0]) and np.array_equal(want[1], got[1])
+
+
+def test_encode_tsv_error_index_is_global_and_first():
+    v = mf.Vocabulary(fx.synthetic_vocab_lines(100))
+    lines = ["w1\tw2\n"] * 5000
+    lines[3100] = "w1\n"
+    lines[4000] = "w1\tw2\tw3\n"
+    with pytest.raises(ColumnCountError) as ei:
+        v.encode_tsv(mf.Kind.COMET_QE, lines, 16, 8, first_index=2048)
+    assert (ei.value.line_index, ei.value.got) == (2048 + 3100, 1)
+
+
+def test_encode_tsv_large_window_matches_encode_batch():
+    v = mf.Vocabulary(fx.synthetic_vocab_lines(5000))
+    lines = ["\t".join(" ".join(f"w{(i * 13 + j * k) % 4995}" for j in range(1 + (i * k) % 70))
+                   for k in (1, 2, 3)) + "\n" for i in range(3000)]
+    recs = [r.field_values(mf.Kind.COMET) for r in mf.records_from_tsv_lines(lines, mf.Kind.COMET)]
+    a = v.encode_batch(mf.Kind.COMET, recs, 48, n_threads=8)
+    b = v.encode_tsv(mf.Kind.COMET, lines, 48, n_threads=8)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
