@@ -475,7 +475,8 @@ struct mfg_ctx {
     att_tc = (d / H == 64 || d / H == 80) && (d % 64 == 0);
     // post-norm bf16 mode: the residual stream travels as bf16 hi/lo pieces of
     // the layer input (~16 significant bits instead of a separate fp32 copy)
-    res_bf16 = !split && !r16 && !pre_norm;
+    // (MFG_BF16_RES32=1 keeps the fp32 residual copy: accuracy A/B runs)
+    res_bf16 = !split && !r16 && !pre_norm && !(getenv("MFG_BF16_RES32") && getenv("MFG_BF16_RES32")[0] == '1');
     make_act(xa, cap_tokens, dp, split || res_bf16);
     make_act(ca, cap_tokens, dp, split);
     make_act(ha, cap_tokens, fp, split);
