@@ -217,8 +217,13 @@ __device__ __forceinline__ void epi_tile_t(const GemmArgs& args, uint32_t tacc, 
       } else {
         float2 y01 = x01, y23 = x23;
         if (EPI == EPI_GELU_SPLIT) {
-          y01 = gelu_tanh2(x01);
-          y23 = gelu_tanh2(x23);
+          if (FMT == FMT_BF16 && args.out_lo == nullptr) {  // bf16 mode: one MUFU per value
+            y01 = gelu_tanh2_bf16out(x01);
+            y23 = gelu_tanh2_bf16out(x23);
+          } else {
+            y01 = gelu_tanh2(x01);
+            y23 = gelu_tanh2(x23);
+          }
         } else if (EPI == EPI_TANH_SPLIT) {
           y01 = make_float2(tanhf(x01.x), tanhf(x01.y));
           y23 = make_float2(tanhf(x23.x), tanhf(x23.y));

@@ -355,6 +355,22 @@ __device__ __forceinline__ float2 gelu_tanh2(float2 x) {
   return fmul2(x, make_float2(fast_rcp(den.x), fast_rcp(den.y)));
 }
 
+// bf16-output variant: 0.5 x (1 + tanh.approx(z)), one MUFU op per value.
+// tanh.approx's error (~2^-11 relative) is far below a bf16 ulp (2^-8); used
+// only where the result is rounded to bf16 (precision "bf16").
+__device__ __forceinline__ float fast_tanh(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float2 gelu_tanh2_bf16out(float2 x) {
+  const float c = 0.7978845608028654f;
+  const float2 z = fmul2(x, ffma2(make_float2(c * 0.044715f, c * 0.044715f), fmul2(x, x),
+                                  make_float2(c, c)));
+  const float2 hx = fmul2(x, make_float2(0.5f, 0.5f));
+  return ffma2(hx, make_float2(fast_tanh(z.x), fast_tanh(z.y)), hx);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
