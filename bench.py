@@ -432,7 +432,10 @@ def run_ours(args, rank, world, local_rank):
                             "head [6144,3072,1024,1]" if args.config == 2 else fx.CONFIG_NAMES[args.config],
                    "records_per_step": R, "tokens_per_step": sum(tokens_per_step[args.warmup:]) / args.steps,
                    "precision": args.precision, "parallelism": f"dp{world} (records sharded)",
-                   "l2": "inputs larger than L2 (1.2 GB weights + GB-scale activations per step)"},
+                   "l2": "inputs larger than L2 ({:.1f} GB of layer weights + GB-scale activations "
+                         "per step)".format(man["n_layers"] * (4 * man["d_model"] ** 2 + 2 * man["d_model"]
+                                                               * man["d_ffn"]) *
+                                            (4 if args.precision in ("fp32", "bf16x3") else 2) / 1e9)},
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": R * 4 + 4,
