@@ -3,6 +3,7 @@ with the repo snapshot to the GPU box).
 
     libmfgpu.so   csrc/*.cu   nvcc -gencode arch=compute_100a,code=sm_100a
     libmfhost.so  csrc/host/*.cpp   g++ (tokenizer, batch plan, packing)
+    mfeval        examples/mfeval.cpp   g++ (C++-only scoring driver over both C-ABIs)
 
 `python -m paper_2408_11853_b200._build [--force]`
 """
@@ -88,9 +89,28 @@ def build_gpu(force=False, verbose=False):
     return GPU_LIB
 
 
+def build_examples(force=False, verbose=False):
+    """lib/mfeval: the C++-only scoring driver over libmfhost + libmfgpu."""
+    src = os.path.join(ROOT, "examples", "mfeval.cpp")
+    exe = os.path.join(LIB, "mfeval")
+    if not os.path.exists(src):
+        return None
+    if not force and not _stale(exe, [src, HOST_LIB, GPU_LIB] + glob.glob(os.path.join(INCLUDE, "*.h"))):
+        return exe
+    tmp = exe + ".tmp"
+    _run([CXX, "-O2", "-std=c++17", "-I" + INCLUDE, src, "-o", tmp, "-L" + LIB, "-lmfhost",
+          "-lmfgpu", "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcudart",
+          "-Wl,-rpath,$ORIGIN", "-Wl,-rpath-link," + os.path.join(CUDA_HOME, "lib64")])
+    os.replace(tmp, exe)
+    if verbose:
+        print("built", exe)
+    return exe
+
+
 def build(force=False, verbose=False):
     build_host(force, verbose)
     build_gpu(force, verbose)
+    build_examples(force, verbose)
 
 
 if __name__ == "__main__":

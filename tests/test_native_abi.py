@@ -56,3 +56,14 @@ def test_host_library_null_safety():
     lib = native.host()
     assert lib.mfh_vocab_size(None) == 0
     assert lib.mfh_plan(None, 0, 0, 1, 1, None) == 2  # mini_batch < 1 rejected
+
+
+def test_mfeval_driver_links_and_reports_usage():
+    """examples/mfeval.cpp links against both C-ABI libraries (no GPU call here)."""
+    exe = ROOT / "paper_2408_11853_b200" / "lib" / "mfeval"
+    assert exe.exists(), "build() produces lib/mfeval"
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 2 and "usage:" in r.stderr
+    nm = subprocess.run(["nm", "-D", "--undefined-only", str(exe)], capture_output=True, text=True).stdout
+    for sym in ("mfh_encode_tsv", "mfh_plan", "mfh_pack_roles", "mfg_create", "mfg_score_batch"):
+        assert sym in nm, sym
