@@ -6,8 +6,10 @@ over the mini-batches of a window (`pkg/src/metricforge/evaluate.py:154-158,
 (`tests/test_evaluate.py:92-98`). Here the workers are processes, one per GPU
 (`torchrun`, RANK / WORLD_SIZE / LOCAL_RANK):
 
-  * every rank tokenises the same input and computes the same global plan
-    (windows -> bit-exact length sort -> mini-batches);
+  * every rank computes the same global plan (windows -> bit-exact length
+    sort -> mini-batches); with TSV lines the tokenisation is sharded too
+    (lengths of 1/w of the lines per rank, all-gathered; then each rank encodes
+    only its own mini-batches' records — `score_sharded_lines`);
   * mini-batches are assigned to ranks longest-processing-time-first on the
     cost  sum_seq (L * c_gemm + L^2 * c_attn)  (round-robin per window would
     always give the longest, sorted-first batch to rank 0);
@@ -108,6 +110,69 @@ def score_sharded(model_score: Callable, vocab, kind, field_texts, max_len, conf
     return flat
 
 
+def score_sharded_lines(model_score: Callable, vocab, kind, lines, max_len, config: BatchConfig,
+                        rank: int, world: int, gather: Optional[Callable] = None,
+                        n_threads: int = 0):
+    """score_sharded for TSV lines with the tokenisation sharded too: rank r
+    encodes lines [n r / w, n (r+1) / w) natively (Vocabulary.encode_tsv) only
+    for their sequence lengths, the lengths are all-gathered, every rank builds
+    the same global plan and LPT assignment, then encodes just the records of
+    its own mini-batches (about 2/w of the host work instead of all of it).
+    The records reach model_score in exactly the order score_sharded uses, so
+    the scores are bitwise the same. Errors: the reference raises the first
+    bad line (ColumnCountError) unless a max_len ValueError comes first, i.e.
+    in an earlier window (`evaluate.py:179-196`); every rank raises the same."""
+    from .errors import ColumnCountError
+
+    kind = Kind.parse(kind)
+    ns = N_SEQUENCES[kind]
+    n = len(lines)
+    if gather is None or world == 1:
+        enc = vocab.encode_tsv(kind, lines, max_len, n_threads)
+        return score_sharded(model_score, vocab, kind, None, max_len, config, rank, world, gather,
+                             n_threads, encoded=(enc, n))
+    a, b = n * rank // world, n * (rank + 1) // world
+    need = 3 if kind is Kind.BLEURT else 2
+    len_err = n > 0 and max_len < need  # raised at window 0's encode by the reference
+    lens, col_err = np.zeros(0, np.int64), None
+    try:
+        _, off = vocab.encode_tsv(kind, lines[a:b], max_len, n_threads, first_index=a)
+        lens = np.diff(off)
+    except ColumnCountError as e:
+        col_err = (e.line_index, e.expected, e.got)
+    except ValueError:
+        if not len_err:
+            raise
+    parts = gather((lens, col_err))
+    cols = [p[1] for p in parts if p[1] is not None]
+    first_col = min(cols) if cols else None
+    if len_err and (first_col is None or first_col[0] >= config.window):
+        what = "BOS, SEP and EOS" if kind is Kind.BLEURT else "BOS and EOS"
+        raise ValueError(f"max_len {max_len} cannot hold {what}")
+    if first_col is not None:
+        raise ColumnCountError(*first_col)
+    seq_lens = np.concatenate([p[0] for p in parts])
+    seq_off = np.zeros(len(seq_lens) + 1, dtype=np.int64)
+    np.cumsum(seq_lens, out=seq_off[1:])
+    order, batches, assign = shard_plan(seq_off, ns, n, config, world)
+    mine = assign[rank]
+    pos = np.concatenate([np.arange(*batches[i]) for i in mine]) if mine else np.zeros(0, np.int64)
+    if len(pos):
+        ids, off = vocab.encode_tsv(kind, [lines[i] for i in order[pos]], max_len, n_threads)
+        packed, cu = pack_roles(ids, off, ns, np.arange(len(pos)))
+        scores = np.asarray(model_score(packed, cu, len(pos)), dtype=np.float32)
+    else:
+        scores = np.zeros(0, np.float32)
+    flat = np.empty(n, dtype=np.float32)
+    seen = 0
+    for p, sc in gather((pos, scores)):
+        flat[order[p]] = sc
+        seen += len(p)
+    if seen != n:
+        raise RuntimeError(f"gathered {seen} scores for {n} records")
+    return flat
+
+
 class DistributedEvaluator:
     """`Evaluator` over all ranks of an initialised torch.distributed group.
 
@@ -138,9 +203,10 @@ class DistributedEvaluator:
     def evaluate_lines(self, lines) -> ScoreReport:
         kind = self.ev.kind
         if isinstance(lines, (list, tuple)) and all(type(l) is str for l in lines):
-            encoded = self.ev.vocab.encode_tsv(kind, lines, self.ev.max_len,
-                                               self.config.tokenizer_threads)
-            n = len(lines)
+            scores = score_sharded_lines(self.ev.model.score_packed, self.ev.vocab, kind, lines,
+                                         self.ev.max_len, self.config.batch, self.rank, self.world,
+                                         self._gather, self.config.tokenizer_threads)
+            return ScoreReport(segment_scores=scores.tolist())
         else:
             recs = [r.field_values(kind, i)
                     for i, r in enumerate(records_from_tsv_lines(lines, kind))]

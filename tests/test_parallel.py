@@ -96,3 +96,67 @@ def test_gloo_two_ranks_equal_single_process(world):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert result[0] == result[1] == solo
+
+
+def _worker_lines(rank, world, port, lines, cfg, result):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2408_11853_b200.errors import ColumnCountError
+        from paper_2408_11853_b200.parallel import score_sharded_lines
+        v = mf.Vocabulary(fx.fixture_vocab_lines())
+
+        def gather(obj):
+            out = [None] * world
+            dist.all_gather_object(out, obj)
+            return out
+
+        try:
+            scores = score_sharded_lines(fake_score, v, "comet", lines, cfg["max_len"],
+                                         mf.BatchConfig(mini_batch=16, maxi_batch_factor=4),
+                                         rank, world, gather)
+            result[rank] = scores.tolist()
+        except ColumnCountError as e:
+            result[rank] = ("ColumnCountError", e.line_index, e.got)
+        except ValueError as e:
+            result[rank] = ("ValueError", str(e))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_ranks(world, lines, cfg):
+    ctx = mp.get_context("spawn")
+    manager = ctx.Manager()
+    result = manager.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_lines, args=(r, world, port, lines, cfg, result))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+        assert p.exitcode == 0
+    return [result[r] for r in range(world)]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_tokenisation_equals_single_process(world):
+    """score_sharded_lines (each rank encodes 1/w of the lines for the plan, then
+    only its own mini-batches) == score_sharded over the whole encoding."""
+    lines = fx.fixture_tsv_lines("comet", 301, seed=5)
+    v = mf.Vocabulary(fx.fixture_vocab_lines())
+    recs = [r.field_values(mf.Kind.COMET) for r in mf.records_from_tsv_lines(lines, mf.Kind.COMET)]
+    solo = score_sharded(fake_score, v, "comet", recs, 128,
+                         mf.BatchConfig(mini_batch=16, maxi_batch_factor=4), 0, 1).tolist()
+    got = _run_ranks(world, lines, {"max_len": 128})
+    assert all(g == solo for g in got)
+
+
+def test_sharded_tokenisation_errors_match_on_every_rank():
+    lines = fx.fixture_tsv_lines("comet", 200, seed=6)
+    lines[150] = "only\ttwo"
+    got = _run_ranks(2, lines, {"max_len": 128})
+    assert got[0] == got[1] == ("ColumnCountError", 150, 2)
+    # max_len too small: raised at window 0 (no bad line there) on every rank
+    got = _run_ranks(2, lines, {"max_len": 1})
+    assert got[0] == got[1] and got[0][0] == "ValueError"
