@@ -13,7 +13,7 @@ def gemm(prec, A, W):
     return out
 rng = np.random.default_rng(0)
 M, N = 256, 512
-for K in (64, 1024, 4096):
+for K in [int(k) for k in os.environ.get("KS", "64,1024,4096").split(",")]:
     A = rng.standard_normal((M, K)).astype(np.float32)
     W = (rng.standard_normal((K, N)) * 0.02).astype(np.float32)
     ref = A.astype(np.float64) @ W.astype(np.float64)
