@@ -72,6 +72,27 @@ bool gemm_uses_pair(int bn) {
 
 int gemm_b_box_rows(int bn) { return gemm_uses_pair(bn) ? 128 : bn; }
 
+// K-chunked accumulation (CTA-pair kernel): the tcgen05 accumulator rounds each
+// MMA's add toward zero, so GEMM error grows with the adds per accumulator
+// (rms 6e-5 of the output std at K = 10240). GEMMs deeper than
+// 4096 (XLM-R XL's FFN2, K = 10240) restart a fresh accumulator every 2048 K
+// and sum the chunks round-to-nearest (rms 1.2e-5); at K <= 4096 the error
+// is small enough for the parity gate and the chunk drains would cost ~1.5 %
+// (measured at config 2). MFG_KCHUNK=E chunks every E elements whenever
+// K > E; MFG_KCHUNK=0 disables. Returns k-blocks per chunk (0 = no chunking).
+int gemm_kchunk_blocks(int K) {
+  static const int env = [] {
+    const char* e = getenv("MFG_KCHUNK");
+    return e ? atoi(e) : -1;
+  }();
+  int elems = env;
+  if (env < 0) elems = K > 4096 ? 2048 : 0;
+  if (elems <= 0 || K <= elems) return 0;
+  return elems / GEMM_BK > 0 ? elems / GEMM_BK : 1;
+}
+
+size_t gemm_partial_floats(int num_sms) { return (size_t)num_sms * GEMM_BM * 256; }
+
 int gemm_pick_bn(int n_pad) {
   if (n_pad % 256 == 0) return 256;
   if (n_pad % 128 == 0) return 128;
@@ -149,6 +170,7 @@ cudaError_t launch_gemm(const CUtensorMap* ah, const CUtensorMap* al, const CUte
   GemmArgs a = a_in;
   a.group_m = group_m;
   const bool split = nsplit == 2;
+  if (!gemm_uses_pair(bn) || a.partial == nullptr) a.kchunk = 0;
   if (gemm_uses_pair(bn))
     return split ? run2_epi<true>(epi, ah, al, bh, bl, a, num_sms, st)
                  : run2_epi<false>(epi, ah, al, bh, bl, a, num_sms, st);

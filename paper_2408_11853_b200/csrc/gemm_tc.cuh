@@ -55,6 +55,11 @@ struct GemmArgs {
   int r16;                   // reference binary16 mode (`encoder.py:120-126`): round the
                              // product to fp16, add the fp16 bias in fp16, round residual
                              // sums to fp16 (bias must hold fp16-representable values)
+  int kchunk;                // CTA-pair kernel: k-blocks per fresh TMEM accumulator (0 = all K).
+  float* partial;            // [gridDim.x][256/4][128][4] fp32: running sum of the finished chunks
+                             // (the tcgen05 accumulator rounds each MMA's add toward zero, so
+                             // error grows with the adds per accumulator; chunk sums are
+                             // added round-to-nearest on the CUDA cores)
 };
 
 __device__ __forceinline__ float round16(float v) { return __half2float(__float2half_rn(v)); }
@@ -121,7 +126,8 @@ __device__ __forceinline__ uint32_t h22u(__half2 h) { return *reinterpret_cast<c
 // sum is one more __hadd2.
 template <int BN, int EPI, int NSUB, int FMT, bool R16>
 __device__ __forceinline__ void epi_tile_t(const GemmArgs& args, uint32_t tacc, int row0, int rows,
-                                           int n0, int half, float* buf, int lane) {
+                                           int n0, int half, float* buf, int lane,
+                                           const float* part_row = nullptr) {
   const int cg = lane & 7;       // transposed phase: 4 columns 4*cg..4*cg+3
   const int rs = lane >> 3;      // row sub-index 0..3
   const bool r16res = EPI == EPI_F32_RES && args.res_hi != nullptr;
@@ -152,6 +158,13 @@ __device__ __forceinline__ void epi_tile_t(const GemmArgs& args, uint32_t tacc, 
     }
     float v[32];
     tmem_ld_32x32(tacc + c, v);
+    if (part_row) {  // earlier K chunks of this tile (this thread's row, columns c..c+31)
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float4 pp = *reinterpret_cast<const float4*>(part_row + (c + i) * GEMM_BM);
+        v[i] += pp.x, v[i + 1] += pp.y, v[i + 2] += pp.z, v[i + 3] += pp.w;
+      }
+    }
 #pragma unroll
     for (int i = 0; i < 32; i += 4)
       *reinterpret_cast<float4*>(buf + lane * GEMM_EPI_STRIDE + (((i >> 2) ^ (lane & 7)) << 2)) =
@@ -255,6 +268,29 @@ __device__ __forceinline__ void epi_tile_t(const GemmArgs& args, uint32_t tacc, 
   }
   if (SPLIT_OUT && FMT == FMT_F16 && args.ovf && (amax >= 65520.f || (hinf & 0x80008000u)))
     atomicOr(args.ovf, 1);
+}
+
+// Finished K chunk of a tile: this thread's TMEM lane (= row) and its columns,
+// stored (first chunk) or added round-to-nearest into the fp32 running sum.
+// Layout [column / 4][row][4]: a warp's float4 access covers 32 consecutive
+// rows = 512 contiguous bytes (part_row points at this thread's row, column 0).
+template <int BN, int NSUB>
+__device__ __forceinline__ void drain_chunk(uint32_t tacc, float* part_row, bool first, int half) {
+#pragma unroll 1
+  for (int c = half * 32; c < BN; c += 32 * NSUB) {
+    float v[32];
+    tmem_ld_32x32(tacc + c, v);
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      float4* p = reinterpret_cast<float4*>(part_row + (c + i) * GEMM_BM);
+      float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      if (!first) {
+        const float4 q = *p;
+        o.x += q.x, o.y += q.y, o.z += q.z, o.w += q.w;
+      }
+      *p = o;
+    }
+  }
 }
 
 // Calls f(integral_constant<FMT>, bool_constant<R16>) for the run-time format:
@@ -556,35 +592,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      const int kc = args.kchunk > 0 ? args.kchunk : kblocks;
       for (int tile = pair; tile < tiles; tile += npairs) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem_base + acc * BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&full[stage], phase);
+        for (int cb = 0; cb < kblocks; cb += kc) {  // one fresh accumulator per K chunk
+          const int ce = min(kblocks, cb + kc);
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
-          const uint64_t ah = umma_desc_sw128(stage_ptr(stage, 0));
-          const uint64_t bh = umma_desc_sw128(stage_ptr(stage, 2));
-          const uint64_t al = SPLIT ? umma_desc_sw128(stage_ptr(stage, 1)) : 0;
-          const uint64_t bl = SPLIT ? umma_desc_sw128(stage_ptr(stage, 3)) : 0;
+          const uint32_t d = tmem_base + acc * BN;
+          for (int kb = cb; kb < ce; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint64_t ah = umma_desc_sw128(stage_ptr(stage, 0));
+            const uint64_t bh = umma_desc_sw128(stage_ptr(stage, 2));
+            const uint64_t al = SPLIT ? umma_desc_sw128(stage_ptr(stage, 1)) : 0;
+            const uint64_t bl = SPLIT ? umma_desc_sw128(stage_ptr(stage, 3)) : 0;
 #pragma unroll
-          for (int k = 0; k < GEMM_BK / 16; ++k) {
-            const uint64_t adv = (uint64_t)(k * 32) >> 4;  // 16 elements along K
-            tc_mma_pair(d, ah + adv, bh + adv, idesc, (kb | k) != 0);
-            if (SPLIT) {
-              tc_mma_pair(d, al + adv, bh + adv, idesc, 1);
-              tc_mma_pair(d, ah + adv, bl + adv, idesc, 1);
+            for (int k = 0; k < GEMM_BK / 16; ++k) {
+              const uint64_t adv = (uint64_t)(k * 32) >> 4;  // 16 elements along K
+              tc_mma_pair(d, ah + adv, bh + adv, idesc, (kb != cb) || k != 0);
+              if (SPLIT) {
+                tc_mma_pair(d, al + adv, bh + adv, idesc, 1);
+                tc_mma_pair(d, ah + adv, bl + adv, idesc, 1);
+              }
+            }
+            tc_commit_pair(&empty[stage], 3);
+            if (++stage == C::STAGES) {
+              stage = 0;
+              phase ^= 1;
             }
           }
-          tc_commit_pair(&empty[stage], 3);
-          if (++stage == C::STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+          tc_commit_pair(&tfull[acc], 3);
+          acc ^= 1;
+          if (acc == 0) acc_phase ^= 1;
         }
-        tc_commit_pair(&tfull[acc], 3);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
       }
     }
   } else if (warp >= 4) {
@@ -593,6 +633,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
     const int half = ew >> 2;      // which 32-column chunks (every EPI_WARPS/4-th) it owns
     float* buf = epi_buf + ew * 32 * GEMM_EPI_STRIDE;
     const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
+    const int kc = args.kchunk > 0 ? args.kchunk : kblocks;
+    const int nch = (kblocks + kc - 1) / kc;
+    float* part_row =
+        nch > 1 ? args.partial + (size_t)blockIdx.x * GEMM_BM * BN + (q * 32 + lane) * 4 : nullptr;
     epi_dispatch(args, [&](auto fmt_c, auto r16_c) {
       int acc = 0;
       uint32_t acc_phase = 0;
@@ -603,17 +647,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
         const int n0 = nt * BN;
         const int row0 = m0 + q * 32;
         const int rows = min(32, args.M - row0);
-        mbar_wait(&tfull[acc], acc_phase);
-        tc_fence_after();
-        if (rows > 0)
-          epi_tile_t<BN, EPI, C::EPI_WARPS / 4, decltype(fmt_c)::value, decltype(r16_c)::value>(
-              args, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, row0, rows, n0, half, buf,
-              lane);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        for (int ch = 0; ch < nch; ++ch) {
+          mbar_wait(&tfull[acc], acc_phase);
+          tc_fence_after();
+          const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+          if (ch + 1 < nch)
+            drain_chunk<BN, C::EPI_WARPS / 4>(tacc, part_row, ch == 0, half);
+          else if (rows > 0)
+            epi_tile_t<BN, EPI, C::EPI_WARPS / 4, decltype(fmt_c)::value, decltype(r16_c)::value>(
+                args, tacc, row0, rows, n0, half, buf, lane, part_row);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+          acc ^= 1;
+          if (acc == 0) acc_phase ^= 1;
+        }
       }
     });
   }

@@ -157,6 +157,7 @@ struct mfg_ctx {
   int64_t cap_tokens = 0;
   int cap_records = 0;
   float *x32 = nullptr, *y32 = nullptr;
+  float* gemm_part = nullptr;  // K-chunk running sums of the CTA-pair GEMM (GemmArgs::partial)
   Act xa, ca, ha, fa, qa;          // qa: Q|K|V pieces [T][qkv_ld]
   // last layer on BOS rows only (one row per sequence): ctx, residual/LN, FFN hidden, Q
   Act cb, xb, hb, qb;
@@ -458,6 +459,7 @@ struct mfg_ctx {
     cap_tokens = pad128(cfg.max_tokens > 0 ? cfg.max_tokens : 262144);
     cap_records = cfg.max_records > 0 ? cfg.max_records : 4096;
     x32 = dalloc<float>((size_t)cap_tokens * dp);
+    gemm_part = dalloc<float>(gemm_partial_floats(num_sms));
     y32 = dalloc<float>((size_t)cap_tokens * dp);
     make_act(qa, cap_tokens, qkv_ld, split);
     {
@@ -518,6 +520,8 @@ struct mfg_ctx {
     g.N = w.Npad;
     g.K = w.Kpad;
     g.bias = w.bias;
+    g.kchunk = gemm_kchunk_blocks(w.Kpad);
+    g.partial = gemm_part;
     g.residual = res;
     g.ldr = ldr;
     if (res16) {
@@ -1062,6 +1066,8 @@ extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, i
     g.fmt = fmt;
     g.ovf = nullptr;
     g.r16 = r16;
+    g.kchunk = gemm_kchunk_blocks(Kp);
+    g.partial = s.alloc<float>(gemm_partial_floats(sms));
     CK(launch_gemm(&mah, split ? &mal : &mah, &mwh, split ? &mwl : &mwh, bn, split ? 2 : 1, epi,
                    g, sms, 0));
     CK(cudaDeviceSynchronize());

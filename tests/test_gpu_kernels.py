@@ -66,6 +66,33 @@ def test_gemm_split_parity(lib, M, N, K, epi, prec):
     assert np.all(np.abs(got - want) <= tol), float(np.abs(got - want).max())
 
 
+@pytest.mark.parametrize("K,epi", [(10240, 0), (4352, 1), (8256, 2)])
+@pytest.mark.parametrize("prec", [0, 1, 3])
+def test_gemm_k_chunked_accumulation(lib, K, epi, prec):
+    """K > 4096: fresh TMEM accumulator every 2048 K, chunks summed round-to-nearest
+    (ragged last chunk at K = 4352 / 8256, residual and GELU epilogues). The
+    error stays at the K = 1024 level instead of growing with K (unchunked, the
+    split GEMM reached rms 6e-5 of the output std at K = 10240)."""
+    rng = np.random.default_rng(K + epi + 7 * prec)
+    M, N = 300, 512
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    W = (rng.standard_normal((K, N)) / math.sqrt(K)).astype(np.float32)
+    if prec == 3:  # reference binary16 mode: operands are exact binary16
+        A = A.astype(np.float16).astype(np.float32)
+        W = W.astype(np.float16).astype(np.float32)
+    b = (0.1 * rng.standard_normal(N)).astype(np.float32)
+    if prec == 3:
+        b = b.astype(np.float16).astype(np.float32)
+    r = rng.standard_normal((M, N)).astype(np.float32)
+    if prec == 3:
+        r = r.astype(np.float16).astype(np.float32)
+    got = _gemm(lib, prec, epi, A, W, b, r)
+    want = _ref(epi, A, W, b, r)
+    rms = float(np.sqrt(np.mean((got - want) ** 2)) / want.std())
+    bound = {0: 1.5e-5, 1: 5e-3, 3: 8e-4}[prec]  # bf16 / binary16 output rounding dominate
+    assert rms <= bound, rms
+
+
 @pytest.mark.parametrize("M,N,K", SHAPES[:6])
 def test_gemm_bf16_mode(lib, M, N, K):
     rng = np.random.default_rng(7 + M)
