@@ -42,6 +42,14 @@ struct Fail {
 
 inline int pad64(int64_t x) { return (int)((x + 63) / 64 * 64); }
 inline int64_t pad128(int64_t x) { return (x + 127) / 128 * 128; }
+// Widths of 1024+ that are not multiples of 256 (RemBERT's d = 1152, 3d = 3456)
+// are padded to 256 so their GEMMs run on the CTA-pair kernel (BN = 256, ~97-99 %
+// tensor pipe) instead of the single-CTA BN = 128 one (~80 %); the padded weight
+// rows and biases are zero, so the padded output columns are 0 and never read.
+inline int padN(int64_t x) {
+  const int p = pad64(x);
+  return (p >= 1024 && p % 256) ? (int)((x + 255) / 256 * 256) : p;
+}
 
 struct DevBuf {
   void* p = nullptr;
@@ -263,7 +271,7 @@ struct mfg_ctx {
     w.N = 0;
     for (auto* m : mats) w.N += (int)m->shape[1];
     w.Kpad = pad64(w.K);
-    w.Npad = pad64(w.N);
+    w.Npad = padN(w.N);
     w.bn = gemm_pick_bn(w.Npad);
     w.hi = dalloc<uint16_t>((size_t)w.Npad * w.Kpad);
     if (split) w.lo = dalloc<uint16_t>((size_t)w.Npad * w.Kpad);
@@ -360,9 +368,9 @@ struct mfg_ctx {
                                           shape_repr(kv.second)};
     }
     d = (int)man.d_model;
-    dp = pad64(d);
+    dp = padN(d);
     f = (int)man.d_ffn;
-    fp = pad64(f);
+    fp = padN(f);
     H = (int)man.n_heads;
     F = feature_multiplier(man.like) * d;
     Fp = pad64(F);
