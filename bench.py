@@ -368,7 +368,8 @@ def run_ours(args, rank, world, local_rank):
     assert all(math.isfinite(v) for v in rep.segment_scores)
 
     # ---------------- reduce over ranks
-    vals = torch.tensor([ms, e2e_s], dtype=torch.float64, device=dev)
+    vals = torch.tensor([ms, e2e_s], dtype=torch.float64,
+                        device="cpu" if dist.is_initialized() and dist.get_backend() == "gloo" else dev)
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     ms_max, e2e_max = float(vals[0]), float(vals[1])
@@ -471,11 +472,18 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    # MFG_BENCH_BACKEND=gloo: code-path check of the multi-rank bench on a box with
+    # fewer GPUs than ranks (ranks share devices; not a measurement)
+    backend = os.environ.get("MFG_BENCH_BACKEND", "nccl")
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "gloo":
+            local_rank %= torch.cuda.device_count()
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:
