@@ -447,7 +447,8 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        base, ref_lines, ref = cpu_baseline(args.config, args.cpu_records, return_scores=True)
+        n_cpu = args.cpu_records or {1: 1024, 5: 4}.get(args.config, 8)
+        base, ref_lines, ref = cpu_baseline(args.config, n_cpu, return_scores=True)
         line["cpu_baseline"] = base
         line["parity"] = parity_report(path, vocab_path, ref_lines, ref, local_rank, args.config)
     print(json.dumps(line), flush=True)
@@ -462,7 +463,9 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16x3", "bf16", "fp16"])
     ap.add_argument("--records-per-step", type=int, default=RECORDS_PER_STEP)
-    ap.add_argument("--cpu-records", type=int, default=8)
+    ap.add_argument("--cpu-records", type=int, default=None,
+                    help="CPU-baseline / parity sample (default: 1024 at config 1, 4 at config 5, "
+                         "else 8 records: ~5-30 s of host work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other-precisions", action="store_true")
     args = ap.parse_args()
