@@ -658,7 +658,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
                 args, tacc, row0, rows, n0, half, buf, lane, part_row);
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+          if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);
           acc ^= 1;
           if (acc == 0) acc_phase ^= 1;
         }

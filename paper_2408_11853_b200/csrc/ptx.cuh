@@ -91,6 +91,13 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// Relaxed remote arrive: no release of this thread's earlier global stores (no
+// membar wait for their completion). For "TMEM accumulator drained" signals,
+// whose only hazard is the TMEM reads, already complete after tcgen05.wait::ld.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
 // TMA load issued by either CTA of a pair; completion bytes go to the leader
 // (rank 0) CTA's barrier at the same offset (peer bit of the address cleared).
 __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map,
