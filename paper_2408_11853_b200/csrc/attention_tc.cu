@@ -214,6 +214,10 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
   constexpr bool TAIL = C::TAIL;
   constexpr bool SPLIT = MODE == 3;     // Q, K, V as hi/lo pairs
   constexpr bool PSPLIT = MODE >= 2;    // P as hi/lo pair
+  constexpr bool DEFER = !SPLIT && DH == 64;  // deferred epilogue (4 O slots of 64 columns)
+  auto oslot = [](int k) { return DEFER ? (k & 3) : (k & 1); };
+  auto opar = [](int k) { return (uint32_t)((DEFER ? (k >> 2) : (k >> 1)) & 1); };
+  auto ocol = [](int k) { return (uint32_t)(DEFER ? 256 + 64 * (k & 3) : 256 + 128 * (k & 1)); };
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
@@ -224,8 +228,12 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
   uint64_t* v_empty = v_full + C::V_ST;     // [V_ST]
   uint64_t* s_full = v_empty + C::V_ST;     // [2]  S(k) in region k&1
   uint64_t* p_full = s_full + 2;            // [2]  P(k) written (256 group threads)
-  uint64_t* o_full = p_full + 2;            // [2]  O(k) done (also: P region free)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_full + 2);
+  // O accumulators: MODE 3 / DH 80 one per region (128 columns, slot k & 1); the
+  // single-plane DH 64 modes (DEFER) have four 64-column slots (k & 3), so a
+  // group runs item k's epilogue after item k+2's softmax, off the S -> P·V chain.
+  uint64_t* o_full = p_full + 2;            // [4]  O(k) done (also: P region free)
+  uint64_t* o_empty = o_full + 4;           // [4]  DEFER: O slot read (256 group threads)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_empty + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -240,7 +248,10 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&p_full[b], 256);
+    }
+    for (int b = 0; b < 4; ++b) {
       mbar_init(&o_full[b], 1);
+      mbar_init(&o_empty[b], 256);
     }
     fence_mbar_init();
   }
@@ -351,7 +362,7 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
         tc_commit(&qk_empty[s]);
       };
       for (int k = 0; k < mine; ++k) {
-        if (k >= 2) mbar_wait(&o_full[k & 1], ((k - 2) >> 1) & 1);  // region free
+        if (k >= 2) mbar_wait(&o_full[oslot(k - 2)], opar(k - 2));  // region free
         mbar_wait(&qk_full[k % C::QK_ST], (k / C::QK_ST) & 1);
         tc_fence_after();
         ATT_TRACE(k, 0);
@@ -372,7 +383,7 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
         const uint32_t idesc64 = idesc_f16kind(128, 64, fmt) | (1u << 16);
         const uint32_t idesc128 = idesc_f16kind(128, 128, fmt) | (1u << 16);
         uint8_t* t = sm + C::QK_ST * C::QK_BYTES + s * C::V_BYTES;
-        const uint32_t tp = tm + b * 128, to = tm + 256 + b * 128;
+        const uint32_t tp = tm + b * 128, to = tm + ocol(k);
         const uint32_t idesc16 = idesc_f16kind(128, 16, fmt) | (1u << 16);
         uint8_t* tt = t + C::NPL_V * ATQ_TILE;
         for (int kk = 0; kk < n16; kk += 16) {
@@ -400,10 +411,11 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
             if (PSPLIT) tc_mma_ts(to, ph_ + 16, vh, idesc64, 1);
           }
         }
-        tc_commit(&o_full[b]);
+        tc_commit(&o_full[oslot(k)]);
         tc_commit(&v_empty[s]);
       };
       for (int k = 0; k < mine; ++k) {
+        if (DEFER && k >= 4) mbar_wait(&o_empty[k & 3], ((k - 4) >> 2) & 1);  // slot read
         mbar_wait(&p_full[k & 1], (k >> 1) & 1);
         mbar_wait(&v_full[k % C::V_ST], (k / C::V_ST) & 1);
         tc_fence_after();
@@ -424,31 +436,87 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
     const int r = q * 32 + hr * 16 + (lane & 15);  // tile row owned by this thread
     const uint32_t lane_off = (uint32_t)(q * 32 + hr * 16) << 16;
     const float c2 = scale * 1.4426950408889634f;  // exp(x*scale) = 2^(x*c2)
-    for (int k = g; k < mine; k += 2) {
-      const int b = g;
+    // This warp's rows lie in one 32-row granule = (part of) one sequence slot:
+    // its keys are [ks, ke) of the tile (warp-uniform).
+    struct Meta {
+      int h, n16, ks, ke, t0;
+      bool active;
+    };
+    auto meta = [&](int k) {
       const int it = item_of(k);
       const AttTile tl = tiles[it / heads];
-      const int h = it % heads;
-      const int n16 = (att_tile_rows(tl) + 15) & ~15;
-      // This warp's rows lie in one 32-row granule = (part of) one sequence
-      // slot: its keys are [ks, ke) of the tile (warp-uniform).
-      int ks = 0, ke = 0, t0 = 0;
-      {
-        int o = 0;
+      Meta m{it % heads, (att_tile_rows(tl) + 15) & ~15, 0, 0, 0, false};
+      int o = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int L = tl.len[j], R = (L + 31) & ~31;
-          if (q * 32 >= o && q * 32 < o + R) {
-            ks = o;
-            ke = o + L;
-            t0 = tl.t0[j];
+      for (int j = 0; j < 4; ++j) {
+        const int L = tl.len[j], R = (L + 31) & ~31;
+        if (q * 32 >= o && q * 32 < o + R) {
+          m.ks = o;
+          m.ke = o + L;
+          m.t0 = tl.t0[j];
+        }
+        o += R;
+      }
+      m.active = m.ke > q * 32 + hr * 16;  // some row of this warp is real
+      return m;
+    };
+    const bool tr = hr == 0 && q == 0 && lane == 0;
+    // ---- epilogue of item k: lanes 0-15 O columns 0..31, lanes 16-31 columns 32..63
+    auto epilogue = [&](int k, const Meta& m, float rsum) {
+      mbar_wait(&o_full[oslot(k)], opar(k));
+      if (tr) ATT_TRACE(k, 4);
+      tc_fence_after();
+      if (m.active) {
+        const int h = m.h, ks = m.ks, ke = m.ke, t0 = m.t0;
+        const uint32_t to = tm + lane_off + ocol(k);
+        const float inv = 1.0f / rsum;
+        const size_t ob = (size_t)(t0 + r - ks) * ldc + h * DH + cp * 32;
+        float v[32];
+        tmem_ld_16x32bx2(to, v);
+        if (SPLIT && !TAIL) {  // O = Ph·Vh + Pl·Vh (columns 0..63) + Ph·Vl (64..127)
+          float w[32];
+          tmem_ld_16x32bx2(to + 64, w);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += w[i];
+        }
+        if (r < ke) {
+          // ctx is a convex combination of range-checked V rows: no fp16 overflow;
+          // 16 pieces = 32 bytes per plane -> one 256-bit store each
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            uint32_t hh[8], ll[8];
+#pragma unroll
+            for (int i = 0; i < 16; i += 2)
+              split2(v[half * 16 + i] * inv, v[half * 16 + i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
+            st_global_256(ch + ob + half * 16, hh);
+            if (SPLIT) st_global_256(cl + ob + half * 16, ll);
           }
-          o += R;
+        }
+        if (TAIL) {  // head dims 64..79: lanes 0-15 dims 64..71, lanes 16-31 dims 72..79
+          float t8[8];
+          tmem_ld_16x32bx2_8(to + 64, t8);
+          if (r < ke) {
+            uint32_t hh[4], ll[4];
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) split2(t8[i] * inv, t8[i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
+            const size_t ot = (size_t)(t0 + r - ks) * ldc + h * DH + 64 + cp * 8;
+            *reinterpret_cast<uint4*>(ch + ot) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
+            if (SPLIT) *reinterpret_cast<uint4*>(cl + ot) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
+          }
         }
       }
-      const bool active = ke > q * 32 + hr * 16;  // some row of this warp is real
+      tc_fence_before();
+      if (DEFER) mbar_arrive(&o_empty[k & 3]);
+      if (tr) ATT_TRACE(k, 5);
+    };
+    Meta prev{};
+    float prev_rsum = 1.f;
+    for (int k = g; k < mine; k += 2) {
+      const int b = g;
+      const Meta m = meta(k);
+      const int n16 = m.n16, ks = m.ks, ke = m.ke;
+      const bool active = m.active;
       mbar_wait(&s_full[b], (k >> 1) & 1);
-      const bool tr = hr == 0 && q == 0 && lane == 0;
       if (tr) ATT_TRACE(k, 2);
       tc_fence_after();
       float rsum = 1.f;
@@ -526,51 +594,15 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
       tc_fence_before();
       mbar_arrive(&p_full[b]);
       if (tr) ATT_TRACE(k, 3);
-      // ---- epilogue: lanes 0-15 O columns 0..31, lanes 16-31 columns 32..63
-      mbar_wait(&o_full[b], (k >> 1) & 1);
-      if (tr) ATT_TRACE(k, 4);
-      tc_fence_after();
-      if (active) {
-        const uint32_t to = tm + lane_off + 256 + b * 128;
-        const float inv = 1.0f / rsum;
-        const size_t ob = (size_t)(t0 + r - ks) * ldc + h * DH + cp * 32;
-        float v[32];
-        tmem_ld_16x32bx2(to, v);
-        if (SPLIT && !TAIL) {  // O = Ph·Vh + Pl·Vh (columns 0..63) + Ph·Vl (64..127)
-          float w[32];
-          tmem_ld_16x32bx2(to + 64, w);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += w[i];
-        }
-        if (r < ke) {
-          // ctx is a convex combination of range-checked V rows: no fp16 overflow;
-          // 16 pieces = 32 bytes per plane -> one 256-bit store each
-#pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            uint32_t hh[8], ll[8];
-#pragma unroll
-            for (int i = 0; i < 16; i += 2)
-              split2(v[half * 16 + i] * inv, v[half * 16 + i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
-            st_global_256(ch + ob + half * 16, hh);
-            if (SPLIT) st_global_256(cl + ob + half * 16, ll);
-          }
-        }
-        if (TAIL) {  // head dims 64..79: lanes 0-15 dims 64..71, lanes 16-31 dims 72..79
-          float t8[8];
-          tmem_ld_16x32bx2_8(tm + lane_off + 256 + b * 128 + 64, t8);
-          if (r < ke) {
-            uint32_t hh[4], ll[4];
-#pragma unroll
-            for (int i = 0; i < 8; i += 2) split2(t8[i] * inv, t8[i + 1] * inv, fmt, hh[i / 2], ll[i / 2]);
-            const size_t ot = (size_t)(t0 + r - ks) * ldc + h * DH + 64 + cp * 8;
-            *reinterpret_cast<uint4*>(ch + ot) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
-            if (SPLIT) *reinterpret_cast<uint4*>(cl + ot) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
-          }
-        }
+      if (!DEFER) {
+        epilogue(k, m, rsum);
+      } else {
+        if (k >= g + 2) epilogue(k - 2, prev, prev_rsum);  // O(k-2) finished during softmax(k)
+        prev = m;
+        prev_rsum = rsum;
       }
-      tc_fence_before();
-      if (tr) ATT_TRACE(k, 5);
     }
+    if (DEFER && mine > g) epilogue(g + 2 * ((mine - 1 - g) / 2), prev, prev_rsum);
   }
 
   tc_fence_before();
