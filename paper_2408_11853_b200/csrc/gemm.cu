@@ -76,9 +76,9 @@ int gemm_b_box_rows(int bn) { return gemm_uses_pair(bn) ? 128 : bn; }
 // MMA's add toward zero, so GEMM error grows with the adds per accumulator
 // (rms 6e-5 of the output std at K = 10240). GEMMs deeper than
 // 4096 (XLM-R XL's FFN2, K = 10240) restart a fresh accumulator every 2048 K
-// and sum the chunks round-to-nearest (rms 1.2e-5); at K <= 4096 the error
-// is small enough for the parity gate and the chunk drains would cost ~1.5 %
-// (measured at config 2). MFG_KCHUNK=E chunks every E elements whenever
+// and sum the chunks round-to-nearest (rms 1.2e-5); XL's K = 2560 GEMMs run
+// in two halves. At config 2's K = 1024 / 4096 the error is small enough for
+// the parity gate and the chunk drains would cost ~1.5 % (measured). MFG_KCHUNK=E chunks every E elements whenever
 // K > E; MFG_KCHUNK=0 disables. Returns k-blocks per chunk (0 = no chunking).
 int gemm_kchunk_blocks(int K) {
   static const int env = [] {
@@ -86,7 +86,10 @@ int gemm_kchunk_blocks(int K) {
     return e ? atoi(e) : -1;
   }();
   int elems = env;
-  if (env < 0) elems = K > 4096 ? 2048 : 0;
+  // default: K > 4096 in 2048-K chunks; 2048 < K <= 4096 in two halves only when
+  // K is not a power of two (XLM-R XL's 2560: measured at no cost, parity 2.5x)
+  if (env < 0)
+    elems = K > 4096 ? 2048 : (K > 2048 && (K & (K - 1)) != 0) ? (K / 2 + 63) / 64 * 64 : 0;
   if (elems <= 0 || K <= elems) return 0;
   return elems / GEMM_BK > 0 ? elems / GEMM_BK : 1;
 }
