@@ -160,3 +160,13 @@ def test_sharded_tokenisation_errors_match_on_every_rank():
     # max_len too small: raised at window 0 (no bad line there) on every rank
     got = _run_ranks(2, lines, {"max_len": 1})
     assert got[0] == got[1] and got[0][0] == "ValueError"
+
+
+def test_sharded_tokenisation_empty_and_tiny_inputs():
+    assert _run_ranks(2, [], {"max_len": 128}) == [[], []]
+    lines = fx.fixture_tsv_lines("comet", 1, seed=3)  # fewer lines than ranks
+    v = mf.Vocabulary(fx.fixture_vocab_lines())
+    recs = [r.field_values(mf.Kind.COMET) for r in mf.records_from_tsv_lines(lines, mf.Kind.COMET)]
+    solo = score_sharded(fake_score, v, "comet", recs, 128,
+                         mf.BatchConfig(mini_batch=16, maxi_batch_factor=4), 0, 1).tolist()
+    assert _run_ranks(3, lines, {"max_len": 128}) == [solo, solo, solo]
