@@ -486,7 +486,8 @@ struct mfg_ctx {
     // post-norm bf16 mode: the residual stream travels as bf16 hi/lo pieces of
     // the layer input (~16 significant bits instead of a separate fp32 copy)
     // (MFG_BF16_RES32=1 keeps the fp32 residual copy: accuracy A/B runs)
-    res_bf16 = !split && !r16 && !pre_norm && !(getenv("MFG_BF16_RES32") && getenv("MFG_BF16_RES32")[0] == '1');
+    const char* res32 = getenv("MFG_BF16_RES32");
+    res_bf16 = !split && !r16 && !pre_norm && !(res32 && res32[0] == '1');
     make_act(xa, cap_tokens, dp, split || res_bf16);
     make_act(ca, cap_tokens, dp, split);
     make_act(ha, cap_tokens, fp, split);
