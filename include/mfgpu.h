@@ -90,6 +90,9 @@ typedef struct {
   int32_t vocab_size, d_model, n_heads, n_layers, d_ffn, max_position, pre_norm;
   int32_t n_roles, n_head_stages, precision, num_sms;
   int64_t device_bytes; /* weights + workspaces resident on the device */
+  /* mfg_create phases (ms): CUDA context, container open (mmap, header, shape
+   * contract), embeddings, layer weights (H2D + transpose/split), head, workspaces */
+  double load_ms[6];
 } mfg_model_info;
 int mfg_get_model_info(const mfg_ctx* ctx, mfg_model_info* out);
 
@@ -103,8 +106,13 @@ typedef struct {
   int64_t class_launches[MFG_NCLASS];
   double class_flops[MFG_NCLASS]; /* algorithmic FLOPs (real, unpadded dims) */
   double class_bytes[MFG_NCLASS]; /* algorithmic HBM bytes */
+  /* fp32-parity path: chunks (and their records) re-scored with bf16 hi/lo pieces
+   * because an activation left the fp16 range (|x| >= 65520) */
+  int64_t fallback_chunks, fallback_records;
 } mfg_stats;
 int mfg_get_stats(const mfg_ctx* ctx, mfg_stats* out);
+/* Switch per-launch CUDA-event timing (mfg_stats.class_ms) on or off between calls. */
+int mfg_set_profile(mfg_ctx* ctx, int32_t enable);
 int mfg_reset_stats(mfg_ctx* ctx);
 
 #ifdef __cplusplus

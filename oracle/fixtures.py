@@ -177,3 +177,29 @@ def synthetic_tsv_lines(cfg, count, seed=TEXT_SEED):
             pos += L
         cols.append(out)
     return ["\t".join(v) for v in zip(*cols)]
+
+
+# --------------------------------------------------------------------------
+# full-size parity subsets (SURVEY.md §8(d) parity protocol)
+# --------------------------------------------------------------------------
+
+PARITY_POOL = 20000
+PARITY_SEED = TEXT_SEED + 31
+PARITY_SIZES = {2: 512, 3: 512, 4: 512, 5: 64}
+
+
+def parity_subset(cfg, n_sub=None, pool=PARITY_POOL, seed=PARITY_SEED):
+    """Length-stratified subset of config `cfg`'s synthetic workload.
+
+    Draws `pool` records from the §8(d) generator, ranks them by total
+    content length (ties by index) and keeps `n_sub` records at evenly spaced
+    ranks, the shortest and the longest included (config 5's 510-token tail
+    reaches the long-sequence attention path). Returned in pool order, as a
+    stream would present them. Returns (pool_indices, lines)."""
+    n_sub = PARITY_SIZES[cfg] if n_sub is None else n_sub
+    lines = synthetic_tsv_lines(cfg, pool, seed=seed)
+    total = np.array([sum(len(c.split()) for c in ln.split("\t")) for ln in lines])
+    ranked = np.lexsort((np.arange(pool), total))
+    picks = ranked[np.rint(np.linspace(0, pool - 1, n_sub)).astype(np.int64)]
+    idx = np.sort(np.unique(picks))
+    return idx.tolist(), [lines[i] for i in idx]

@@ -39,6 +39,9 @@ enum EpiMode : int {
 struct GemmArgs {
   int M, N, K;               // M real rows; N, K padded (N % BN == 0, K % 64 == 0)
   const float* bias;         // [N]
+  const float* alpha;        // [N] or null: out = acc * alpha + bias. The fp32-parity path
+                             // stores each weight column pre-scaled by a power of two
+                             // (largest |w| in [2^14, 2^15)), so alpha = 2^-e is exact
   const float* residual;     // [M][ldr] (EPI_F32_RES), fp32 ...
   int ldr;
   const uint16_t* res_hi;    // ... or, when non-null, 16-bit hi (+ lo) pieces [M][ldr]
@@ -171,6 +174,9 @@ __device__ __forceinline__ void epi_tile_t(const GemmArgs& args, uint32_t tacc, 
           make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
     __syncwarp();
     const float4 b = *reinterpret_cast<const float4*>(args.bias + col);
+    // fma(acc, 1, b) == acc + b bitwise, so unscaled weights take the same path
+    const float4 al = args.alpha ? *reinterpret_cast<const float4*>(args.alpha + col)
+                                 : make_float4(1.f, 1.f, 1.f, 1.f);
     const __half2 bh01 = __floats2half2_rn(b.x, b.y), bh23 = __floats2half2_rn(b.z, b.w);
     auto row = [&](int it) {
       const int r = it * 4 + rs;
@@ -198,8 +204,8 @@ __device__ __forceinline__ void epi_tile_t(const GemmArgs& args, uint32_t tacc, 
         x01 = __half22float2(h01);
         x23 = __half22float2(h23);
       } else {
-        x01 = fadd2(make_float2(s4.x, s4.y), make_float2(b.x, b.y));
-        x23 = fadd2(make_float2(s4.z, s4.w), make_float2(b.z, b.w));
+        x01 = ffma2(make_float2(s4.x, s4.y), make_float2(al.x, al.y), make_float2(b.x, b.y));
+        x23 = ffma2(make_float2(s4.z, s4.w), make_float2(al.z, al.w), make_float2(b.z, b.w));
       }
       if (EPI == EPI_F32 || EPI == EPI_F32_RES) {
         if (EPI == EPI_F32_RES) {

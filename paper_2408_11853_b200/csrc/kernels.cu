@@ -476,12 +476,14 @@ __global__ void features_kernel(const float* __restrict__ x, int ld, int d, int 
 // padding untouched (destination is zero-initialised).
 __global__ void transpose_split_kernel(const float* __restrict__ w, int K, int N,
                                        uint16_t* __restrict__ hi, uint16_t* __restrict__ lo,
-                                       int ldk, int row0, int fmt, int* ovf) {
+                                       int ldk, int row0, int fmt, int* ovf,
+                                       const float* __restrict__ alpha) {
   __shared__ float tile[32][33];
   const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  const float s = alpha && n0 + threadIdx.x < N ? __frcp_rn(alpha[n0 + threadIdx.x]) : 1.f;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int k = k0 + i, n = n0 + threadIdx.x;
-    tile[i][threadIdx.x] = (k < K && n < N) ? w[(size_t)k * N + n] : 0.f;
+    tile[i][threadIdx.x] = (k < K && n < N) ? w[(size_t)k * N + n] * s : 0.f;
   }
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -489,6 +491,37 @@ __global__ void transpose_split_kernel(const float* __restrict__ w, int K, int N
     if (n < N && k < K)
       store_split(hi, lo, (size_t)(row0 + n) * ldk + k, tile[threadIdx.x][i], fmt, ovf);
   }
+}
+
+// Column maxima of |w| as float bits (non-negative floats order like their bits),
+// accumulated with atomicMax into alpha_bits[N] (zeroed by the caller).
+__global__ void colmax_kernel(const float* __restrict__ w, int K, int N,
+                              unsigned* __restrict__ alpha_bits) {
+  __shared__ unsigned part[8][32];
+  const int n = blockIdx.x * 32 + threadIdx.x;
+  unsigned m = 0;
+  if (n < N)
+    for (int k = blockIdx.y * 256 + threadIdx.y; k < min(K, (int)blockIdx.y * 256 + 256); k += 8)
+      m = max(m, __float_as_uint(w[(size_t)k * N + n]) & 0x7fffffffu);
+  part[threadIdx.y][threadIdx.x] = m;
+  __syncthreads();
+  if (threadIdx.y == 0 && n < N) {
+    for (int i = 1; i < 8; ++i) m = max(m, part[i][threadIdx.x]);
+    atomicMax(alpha_bits + n, m);
+  }
+}
+
+// max bits -> alpha = 2^(e - 14) (see launch_weight_scales)
+__global__ void colscale_kernel(float* __restrict__ alpha, int N) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const unsigned bits = __float_as_uint(alpha[n]);
+  float a = 1.f;
+  if (bits != 0 && bits < 0x7f800000u) {
+    const int e = max(-100, (int)(bits >> 23) - 127);  // floor(log2 max); subnormals clamp
+    a = __uint_as_float((unsigned)(e - 14 + 127) << 23);
+  }
+  alpha[n] = a;
 }
 
 // BOS rows -> compact sequence-indexed rows (the last layer only feeds pooling,
@@ -617,9 +650,19 @@ cudaError_t launch_features(const float* x, int ld, int d, int kind, const int32
 }
 
 cudaError_t launch_transpose_split(const float* w, int K, int N, uint16_t* hi, uint16_t* lo,
-                                   int ldk, int row0, int fmt, int* ovf, cudaStream_t st) {
+                                   int ldk, int row0, int fmt, int* ovf, cudaStream_t st,
+                                   const float* alpha) {
   dim3 grid((N + 31) / 32, (K + 31) / 32), block(32, 8);
-  transpose_split_kernel<<<grid, block, 0, st>>>(w, K, N, hi, lo, ldk, row0, fmt, ovf);
+  transpose_split_kernel<<<grid, block, 0, st>>>(w, K, N, hi, lo, ldk, row0, fmt, ovf, alpha);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_weight_scales(const float* w, int K, int N, float* alpha, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(alpha, 0, (size_t)N * sizeof(float), st);
+  if (e != cudaSuccess) return e;
+  dim3 grid((N + 31) / 32, (K + 255) / 256), block(32, 8);
+  colmax_kernel<<<grid, block, 0, st>>>(w, K, N, reinterpret_cast<unsigned*>(alpha));
+  colscale_kernel<<<(N + 255) / 256, 256, 0, st>>>(alpha, N);
   return cudaGetLastError();
 }
 

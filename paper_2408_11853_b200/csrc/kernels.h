@@ -60,8 +60,17 @@ cudaError_t launch_bos_attention(const uint16_t* qbh, const uint16_t* qbl, int l
 cudaError_t launch_features(const float* x, int ld, int d, int kind, const int32_t* cu, int n,
                             uint16_t* fh, uint16_t* fl, int ldf, int fmt, int* ovf,
                             cudaStream_t st);
+// Wᵀ rows row0.. = columns of w [K][N], split into 16-bit hi/lo pieces; with
+// `alpha` (non-null) column n is multiplied by 1 / alpha[n] first (exact: powers of two).
 cudaError_t launch_transpose_split(const float* w, int K, int N, uint16_t* hi, uint16_t* lo,
-                                   int ldk, int row0, int fmt, int* ovf, cudaStream_t st);
+                                   int ldk, int row0, int fmt, int* ovf, cudaStream_t st,
+                                   const float* alpha = nullptr);
+// Per-column power-of-two prescale of w [K][N] for the fp16 hi/lo split:
+// alpha[n] = 2^(e_n - 14) where 2^e_n <= max_k |w[k][n]| < 2^(e_n + 1), so the
+// scaled column's largest element lies in [2^14, 2^15) (no fp16 overflow, the lo
+// piece stays normal down to 2^-29 of the column max). Zero / non-finite columns
+// get alpha = 1 (non-finite ones then flag the fp16 overflow as before).
+cudaError_t launch_weight_scales(const float* w, int K, int N, float* alpha, cudaStream_t st);
 // Copy the BOS row (cu[s]) of each sequence to compact row s (16-bit planes and/or fp32).
 cudaError_t launch_gather_bos(const int32_t* cu, int nseq, int d, const uint16_t* sh,
                               const uint16_t* sl, int lds, const float* s32, int ld32, uint16_t* dh,

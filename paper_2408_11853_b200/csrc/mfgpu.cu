@@ -60,6 +60,7 @@ struct DevBuf {
 struct Weight {
   uint16_t *hi = nullptr, *lo = nullptr;
   float* bias = nullptr;
+  float* alpha = nullptr;  // fp32-parity path: per-column 2^-e undoing the weight prescale
   int N = 0, K = 0, Npad = 0, Kpad = 0, bn = 64;
   CUtensorMap mh{}, ml{};
 };
@@ -147,6 +148,11 @@ struct mfg_ctx {
   bool split = true, pre_norm = false, profile = false;
   bool res_bf16 = false;   // bf16 mode: residual stream as bf16 hi/lo pieces (post-norm)
   bool r16 = false;        // reference binary16 mode: every tensor and activation is fp16
+  bool prescale = true;
+  // load phases (ms): context, open (mmap + header + shape contract), embeddings,
+  // layer weights (H2D + transpose/split), head weights, workspaces
+  double load_ms[6] = {0, 0, 0, 0, 0, 0};    // fp32-parity path: power-of-two weight column prescale
+                           // (MFG_WEIGHT_PRESCALE=0 disables it: accuracy A/B only)
   int fmt = FMT_F16;       // 16-bit operand format of every GEMM operand
   int* d_ovf = nullptr;    // fp16 range overflow flag (set by any producer)
   int* h_ovf = nullptr;
@@ -275,14 +281,21 @@ struct mfg_ctx {
     w.bn = gemm_pick_bn(w.Npad);
     w.hi = dalloc<uint16_t>((size_t)w.Npad * w.Kpad);
     if (split) w.lo = dalloc<uint16_t>((size_t)w.Npad * w.Kpad);
+    // fp16 hi/lo pieces: every weight column is pre-scaled by a power of two so its
+    // largest element sits in [2^14, 2^15): any finite weight fits the fp16 range and
+    // the lo piece keeps 11 bits for elements down to 2^-15 of the column max (the
+    // epilogue multiplies the accumulator back by alpha, exactly)
+    if (split && fmt == FMT_F16 && prescale) w.alpha = dalloc<float>(w.Npad);
     int row0 = 0;
     for (auto* m : mats) {
       const float* src = host_f32(*m, host_tmp);
       // two device staging halves alternate so the next matrix's H2D overlaps this transpose
       float* stg = staging_dev + (stage_flip ^= 1) * staging_half;
       up->upload(stg, src, m->numel() * 4);
+      if (w.alpha)
+        CK(launch_weight_scales(stg, (int)m->shape[0], (int)m->shape[1], w.alpha + row0, st));
       CK(launch_transpose_split(stg, (int)m->shape[0], (int)m->shape[1], w.hi, w.lo,
-                                w.Kpad, row0, fmt, d_ovf, st));
+                                w.Kpad, row0, fmt, d_ovf, st, w.alpha ? w.alpha + row0 : nullptr));
       row0 += (int)m->shape[1];
     }
     w.bias = dalloc<float>(w.Npad);
@@ -339,17 +352,23 @@ struct mfg_ctx {
 
   void build(const mfg_config& cfg) {
     // MFG_LOAD_TRACE=1: phase timings of the weight upload on stderr
+    // (always recorded per phase in load_ms, mfg_model_info)
     const bool trace = getenv("MFG_LOAD_TRACE") != nullptr;
     auto clk = [] { return std::chrono::steady_clock::now(); };
     auto t_start = clk();
-    auto lap = [&](const char* what) {
-      if (!trace) return;
+    auto t_prev = t_start;
+    auto lap = [&](const char* what, int phase = -1) {
       cudaStreamSynchronize(st);
-      fprintf(stderr, "mfg load: %-12s %8.1f ms\n", what,
-              std::chrono::duration<double, std::milli>(clk() - t_start).count());
+      auto now = clk();
+      if (phase >= 0) load_ms[phase] += std::chrono::duration<double, std::milli>(now - t_prev).count();
+      t_prev = now;
+      if (trace)
+        fprintf(stderr, "mfg load: %-12s %8.1f ms\n", what,
+                std::chrono::duration<double, std::milli>(now - t_start).count());
     };
     Container c(cfg.container_path);
-    lap("open");
+    lap("open", 1);
+    if (const char* e = getenv("MFG_WEIGHT_PRESCALE")) prescale = e[0] != '0';
     man = c.manifest();
     if (man.like == "comet-qe") { kind = 0; n_roles = 2; }
     else if (man.like == "comet") { kind = 1; n_roles = 3; }
@@ -393,9 +412,9 @@ struct mfg_ctx {
     d_ovf = dalloc<int>(1);
     CK(cudaMallocHost(&h_ovf, sizeof(int)));
     try {
-      lap("setup");
+      lap("setup", 1);
       tok = upload_vec(*c.find("emb.tok"));
-      lap("emb.tok");
+      lap("emb.tok", 2);
       pos = upload_vec(*c.find("emb.pos"));
       layers.resize(man.n_layers);
       for (int i = 0; i < man.n_layers; ++i) {
@@ -412,7 +431,7 @@ struct mfg_ctx {
         L.g2 = upload_vec(*T(".norm2.g"));
         L.b2 = upload_vec(*T(".norm2.b"));
       }
-      lap("layers");
+      lap("layers", 3);
       // last layer's Q / K|V views of the fused QKV weight (needs d % 64 == 0 so the
       // split falls on a padded-row boundary, and tile-aligned N for both parts)
       if (!layers.empty() && d % 64 == 0) {
@@ -425,6 +444,7 @@ struct mfg_ctx {
           v.hi = w.hi + (size_t)row0 * w.Kpad;
           v.lo = w.lo ? w.lo + (size_t)row0 * w.Kpad : nullptr;
           v.bias = w.bias + row0;
+          v.alpha = w.alpha ? w.alpha + row0 : nullptr;
           v.N = n;
           v.K = w.K;
           v.Npad = n;
@@ -458,11 +478,10 @@ struct mfg_ctx {
     CK(cudaFree(staging));
     CK(cudaMemcpy(h_ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost));
     if (*h_ovf)
-      throw Fail{MFG_ERR_USAGE, "a weight exceeds the fp16 range of the fp32-parity path "
-                                "(|w| >= 65520); use precision bf16x3"};
+      throw Fail{MFG_ERR_USAGE, "a weight is not finite (inf or nan)"};
     qkv_ld = layers.empty() ? pad64(3 * d) : layers[0].qkv.Npad;
 
-    lap("weights");
+    lap("weights", 4);
     // workspaces
     cap_tokens = pad128(cfg.max_tokens > 0 ? cfg.max_tokens : 262144);
     cap_records = cfg.max_records > 0 ? cfg.max_records : 4096;
@@ -517,7 +536,7 @@ struct mfg_ctx {
     CK(cudaMallocHost(&h_scores, cap_records * 4));
     CK(cudaEventCreate(&ev0));
     CK(cudaEventCreate(&ev1));
-    CK(cudaStreamSynchronize(st));
+    lap("workspaces", 5);
   }
 
   // ---------------------------------------------------------------- forward
@@ -529,6 +548,7 @@ struct mfg_ctx {
     g.N = w.Npad;
     g.K = w.Kpad;
     g.bias = w.bias;
+    g.alpha = w.alpha;
     g.kchunk = gemm_kchunk_blocks(w.Kpad);
     g.partial = gemm_part;
     g.residual = res;
@@ -704,15 +724,77 @@ struct mfg_ctx {
     }
   }
 
-  void check_flag() {
+  // Returns true when an fp16 operand piece overflowed (|x| >= 65520) in the chunk.
+  bool check_flag() {
     CK(cudaMemcpyAsync(h_ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (*h_ovf & 2)
       throw Fail{MFG_ERR_USAGE,
                  "token id out of range for vocab_size " + std::to_string(man.vocab_size)};
-    if (*h_ovf & 1)
-      throw Fail{MFG_ERR_RUNTIME, "an activation exceeded the fp16 range of the fp32-parity path "
-                                  "(|x| >= 65520); rerun with precision bf16x3"};
+    return (*h_ovf & 1) != 0;
+  }
+
+  // ---------------------------------------------------------------- range fallback
+  // The fp32-parity path keeps activations as fp16 hi/lo pieces; an activation
+  // beyond the fp16 range (the reference computes in fp32 and has no such limit,
+  // `encoder.py:120-130`) re-scores that chunk on a twin context with bf16 hi/lo
+  // pieces (fp32 range, ~16 significant bits, 3 MMAs per k-step), built on first
+  // use from the same container. Counted in mfg_stats.fallback_*.
+  mfg_config cfg_copy{};
+  std::string cfg_path;
+  mfg_ctx* twin = nullptr;
+
+  void rescore_chunk_bf16x3(int m, int64_t T, const int32_t* chunk_ids, float* out, bool device_io) {
+    if (!twin) {
+      mfg_config tc = cfg_copy;
+      tc.container_path = cfg_path.c_str();
+      tc.precision = MFG_PREC_BF16X3;
+      tc.profile = 0;
+      twin = new mfg_ctx();
+      try {
+        twin->init(tc);
+      } catch (...) {
+        delete twin;
+        twin = nullptr;
+        throw;
+      }
+    }
+    twin->st = st;
+    std::vector<int64_t> cu64((size_t)m * n_roles + 1);
+    for (size_t i = 0; i < cu64.size(); ++i) cu64[i] = h_cu[i];
+    if (cu64.back() != T) throw Fail{MFG_ERR_RUNTIME, "fallback chunk bookkeeping"};
+    const int64_t launches0 = twin->stats.kernel_launches;
+    twin->score(m, n_roles, chunk_ids, cu64.data(), out, device_io);
+    stats.kernel_launches += twin->stats.kernel_launches - launches0;
+    stats.fallback_chunks += 1;
+    stats.fallback_records += m;
+  }
+
+  void init(const mfg_config& cfg) {
+    if (cfg.precision < MFG_PREC_FP32 || cfg.precision > MFG_PREC_FP16)
+      throw Fail{MFG_ERR_USAGE, "unknown precision " + std::to_string(cfg.precision)};
+    cfg_copy = cfg;
+    cfg_path = cfg.container_path;
+    device = cfg.device;
+    precision = cfg.precision;
+    split = cfg.precision == MFG_PREC_FP32 || cfg.precision == MFG_PREC_BF16X3;
+    r16 = cfg.precision == MFG_PREC_FP16;
+    fmt = (cfg.precision == MFG_PREC_FP32 || r16) ? FMT_F16 : FMT_BF16;
+    profile = cfg.profile != 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    CK(cudaSetDevice(device));
+    CK(cudaFree(nullptr));  // create the primary context here (timed as its own phase)
+    int major = 0, minor = 0;
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    if (major != 10 || minor != 0)
+      throw Fail{MFG_ERR_RUNTIME, "libmfgpu is built for sm_100a (B200); device is sm_" +
+                                      std::to_string(major) + std::to_string(minor)};
+    CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaStreamCreateWithFlags(&own_st, cudaStreamNonBlocking));
+    st = own_st;
+    load_ms[0] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    build(cfg);
   }
 
   // ids / out are host pointers (device_io == false) or device pointers (true);
@@ -789,11 +871,11 @@ struct mfg_ctx {
       forward_chunk(m, T, (int64_t)v_work.size(), (int)v_tiles.size(), sum_l2, (int)max_l);
       if (device_io) {
         CK(cudaMemcpyAsync(out + r0, dscores, m * 4, cudaMemcpyDeviceToDevice, st));
-        check_flag();
+        if (check_flag()) rescore_chunk_bf16x3(m, T, d_ids, out + r0, true);
       } else {
         CK(cudaMemcpyAsync(h_scores, dscores, m * 4, cudaMemcpyDeviceToHost, st));
-        check_flag();
-        memcpy(out + r0, h_scores, m * 4);
+        if (check_flag()) rescore_chunk_bf16x3(m, T, h_ids, out + r0, false);
+        else memcpy(out + r0, h_scores, m * 4);
       }
       stats.tokens += T;
       stats.chunks += 1;
@@ -811,6 +893,7 @@ struct mfg_ctx {
 
   ~mfg_ctx() {
     if (st) cudaStreamSynchronize(st);
+    delete twin;
     for (void* p : allocs) cudaFree(p);
     if (h_ids) cudaFreeHost(h_ids);
     if (h_cu) cudaFreeHost(h_cu);
@@ -837,25 +920,7 @@ extern "C" int mfg_create(const mfg_config* cfg, mfg_ctx** out) {
   *out = nullptr;
   mfg_ctx* c = new mfg_ctx();
   try {
-    if (cfg->precision < MFG_PREC_FP32 || cfg->precision > MFG_PREC_FP16)
-      throw Fail{MFG_ERR_USAGE, "unknown precision " + std::to_string(cfg->precision)};
-    c->device = cfg->device;
-    c->precision = cfg->precision;
-    c->split = cfg->precision == MFG_PREC_FP32 || cfg->precision == MFG_PREC_BF16X3;
-    c->r16 = cfg->precision == MFG_PREC_FP16;
-    c->fmt = (cfg->precision == MFG_PREC_FP32 || c->r16) ? FMT_F16 : FMT_BF16;
-    c->profile = cfg->profile != 0;
-    CK(cudaSetDevice(c->device));
-    int major = 0, minor = 0;
-    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c->device));
-    CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, c->device));
-    if (major != 10 || minor != 0)
-      throw Fail{MFG_ERR_RUNTIME, "libmfgpu is built for sm_100a (B200); device is sm_" +
-                                      std::to_string(major) + std::to_string(minor)};
-    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
-    CK(cudaStreamCreateWithFlags(&c->own_st, cudaStreamNonBlocking));
-    c->st = c->own_st;
-    c->build(*cfg);
+    c->init(*cfg);
   } catch (const Fail& f) {
     delete c;
     return set_global(f.code, f.msg);
@@ -951,12 +1016,22 @@ extern "C" int mfg_get_model_info(const mfg_ctx* c, mfg_model_info* o) {
   o->precision = c->precision;
   o->num_sms = c->num_sms;
   o->device_bytes = c->device_bytes;
+  for (int i = 0; i < 6; ++i) o->load_ms[i] = c->load_ms[i];
   return MFG_OK;
 }
 
 extern "C" int mfg_get_stats(const mfg_ctx* c, mfg_stats* o) {
   if (!c || !o) return MFG_ERR_USAGE;
   *o = c->stats;
+  return MFG_OK;
+}
+
+extern "C" int mfg_set_profile(mfg_ctx* c, int32_t enable) {
+  if (!c) return set_global(MFG_ERR_USAGE, "null context");
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->st);
+  if (c->profile && !enable) c->collect_profile();
+  c->profile = enable != 0;
   return MFG_OK;
 }
 
@@ -1039,7 +1114,12 @@ extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, i
     const int64_t tot = (int64_t)M * K;
     split_rows_kernel<<<(unsigned)((tot + 255) / 256), 256>>>(dA, M, K, ah, al, Kp, fmt);
     CK(cudaGetLastError());
-    CK(launch_transpose_split(dW, K, N, wh, wl, Kp, 0, fmt, nullptr, 0));
+    float* dal = nullptr;
+    if (split && fmt == FMT_F16) {  // the engine's per-column weight prescale
+      dal = s.alloc<float>(Np);
+      CK(launch_weight_scales(dW, K, N, dal, 0));
+    }
+    CK(launch_transpose_split(dW, K, N, wh, wl, Kp, 0, fmt, nullptr, 0, dal));
     float* db = s.alloc<float>(Np);
     if (bias) {
       std::vector<float> b(bias, bias + N);
@@ -1065,6 +1145,7 @@ extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, i
     g.N = Np;
     g.K = Kp;
     g.bias = db;
+    g.alpha = dal;
     g.residual = dr;
     g.ldr = Np;
     g.out_f32 = d32;

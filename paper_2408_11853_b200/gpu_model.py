@@ -149,12 +149,21 @@ class GpuScoringModel:
         s = native.MfgStats()
         self._lib.mfg_get_stats(self._h, C.byref(s))
         out = {k: getattr(s, k) for k in ("device_ms", "calls", "records", "tokens", "chunks",
-                                           "kernel_launches")}
+                                           "kernel_launches", "fallback_chunks",
+                                           "fallback_records")}
         out["classes"] = {
             name: {"ms": s.class_ms[i], "launches": s.class_launches[i],
                    "flops": s.class_flops[i], "bytes": s.class_bytes[i]}
             for i, name in enumerate(native.CLASS_NAMES)}
         return out
+
+    def set_profile(self, enable: bool):
+        """Per-launch CUDA-event timing on / off (class_ms in stats())."""
+        self._lib.mfg_set_profile(self._h, int(bool(enable)))
+
+    def load_phases(self) -> dict:
+        """mfg_create phase timings in ms (context, open, embeddings, layers, head, workspaces)."""
+        return {k: float(self.info.load_ms[i]) for i, k in enumerate(native.LOAD_PHASES)}
 
     def reset_stats(self):
         self._lib.mfg_reset_stats(self._h)

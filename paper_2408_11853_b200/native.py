@@ -75,7 +75,9 @@ class MfgConfig(C.Structure):
 class MfgModelInfo(C.Structure):
     _fields_ = [(n, i32) for n in ("kind", "vocab_size", "d_model", "n_heads", "n_layers", "d_ffn",
                                    "max_position", "pre_norm", "n_roles", "n_head_stages",
-                                   "precision", "num_sms")] + [("device_bytes", i64)]
+                                   "precision", "num_sms")] + [("device_bytes", i64),
+                                                               ("load_ms", C.c_double * 6)]
+LOAD_PHASES = ("context", "open", "embeddings", "layers", "head", "workspaces")
 
 
 NCLASS = 8
@@ -86,7 +88,8 @@ class MfgStats(C.Structure):
     _fields_ = [("device_ms", C.c_double), ("calls", i64), ("records", i64), ("tokens", i64),
                 ("chunks", i64), ("kernel_launches", i64),
                 ("class_ms", C.c_double * NCLASS), ("class_launches", i64 * NCLASS),
-                ("class_flops", C.c_double * NCLASS), ("class_bytes", C.c_double * NCLASS)]
+                ("class_flops", C.c_double * NCLASS), ("class_bytes", C.c_double * NCLASS),
+                ("fallback_chunks", i64), ("fallback_records", i64)]
 
 
 def gpu():
@@ -112,6 +115,8 @@ def gpu():
             lib.mfg_get_model_info.restype = C.c_int
             lib.mfg_get_stats.argtypes = [C.c_void_p, C.POINTER(MfgStats)]
             lib.mfg_get_stats.restype = C.c_int
+            lib.mfg_set_profile.argtypes = [C.c_void_p, i32]
+            lib.mfg_set_profile.restype = C.c_int
             lib.mfg_reset_stats.argtypes = [C.c_void_p]
             lib.mfg_reset_stats.restype = C.c_int
             lib.mfgt_gemm.argtypes = [i32, i32, i32, i32, i32, f32p, f32p, f32p, f32p, f32p]

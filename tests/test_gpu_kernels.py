@@ -195,3 +195,25 @@ def test_gemm_fp16_reference_mode(lib, M, N, K, epi):
     d = np.abs(got - want)
     assert np.all(d <= 3 * ulp + 1e-7), float((d / ulp).max())
     assert np.mean(d == 0) > 0.97
+
+
+@pytest.mark.parametrize("k", [-14, -7, 17])
+@pytest.mark.parametrize("epi", [0, 1])
+def test_gemm_weight_prescale_is_scale_equivariant(lib, k, epi):
+    """fp32-parity GEMM: with the per-column power-of-two weight prescale,
+    weights and bias times 2^k give exactly 2^k times the output — tiny weights
+    (2^-14 ~ 6e-5: unscaled, their fp16 lo pieces would be subnormal) and huge
+    ones (2^17: beyond the fp16 range, which used to fail the load) keep the
+    unit-scale precision bit for bit."""
+    rng = np.random.default_rng(100 + k + epi)
+    M, N, K = 300, 384, 1024
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    W = (rng.standard_normal((K, N)) / math.sqrt(K)).astype(np.float32)
+    b = (0.1 * rng.standard_normal(N)).astype(np.float32)
+    r = rng.standard_normal((M, N)).astype(np.float32)
+    s = np.float32(2.0 ** k)
+    base = _gemm(lib, 0, epi, A, W, b, r)
+    scaled = _gemm(lib, 0, epi, A, W * s, b * s, r * s)  # epi 1: residual scaled too
+    assert np.array_equal(scaled, base * s)
+    rel = float(np.abs(base - _ref(epi, A, W, b, r)).max() / np.abs(base).max())
+    assert rel <= 2e-5, rel

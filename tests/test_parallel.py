@@ -98,28 +98,42 @@ def test_gloo_two_ranks_equal_single_process(world):
     assert result[0] == result[1] == solo
 
 
-def _worker_lines(rank, world, port, lines, cfg, result):
+def _worker_stream(rank, world, port, lines, cfg, result):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2408_11853_b200.errors import ColumnCountError
-        from paper_2408_11853_b200.parallel import score_sharded_lines
+        from paper_2408_11853_b200.parallel import Comm, _rounds_from_lines, stream_sharded
         v = mf.Vocabulary(fx.fixture_vocab_lines())
+        batch = mf.BatchConfig(mini_batch=16, maxi_batch_factor=4)
+        per_round = batch.window * cfg.get("stream_windows", 2)
+        consumed = [0]
+        trace = []
 
-        def gather(obj):
-            out = [None] * world
-            dist.all_gather_object(out, obj)
-            return out
+        def gen():  # a lazy source: counts how far the coordinator has read
+            for ln in lines:
+                consumed[0] += 1
+                yield ln
 
+        def score(ids, cu, n):
+            trace.append(consumed[0])
+            if cfg.get("fail_rank") == rank:
+                raise RuntimeError(f"device failure on rank {rank}")
+            return fake_score(ids, cu, n)
+
+        rounds = (_rounds_from_lines(v, mf.Kind.COMET, gen(), cfg["max_len"], per_round, 0)
+                  if rank == 0 else None)
         try:
-            scores = score_sharded_lines(fake_score, v, "comet", lines, cfg["max_len"],
-                                         mf.BatchConfig(mini_batch=16, maxi_batch_factor=4),
-                                         rank, world, gather)
+            scores = stream_sharded(score, rounds, "comet", batch, Comm(rank, world))
             result[rank] = scores.tolist()
-        except ColumnCountError as e:
+        except mf.errors.ColumnCountError as e:
             result[rank] = ("ColumnCountError", e.line_index, e.got)
         except ValueError as e:
             result[rank] = ("ValueError", str(e))
+        except RuntimeError as e:
+            result[rank] = ("RuntimeError", str(e))
+        if rank == 0:
+            result["trace"] = trace
+            result["per_round"] = per_round
     finally:
         dist.destroy_process_group()
 
@@ -129,44 +143,70 @@ def _run_ranks(world, lines, cfg):
     manager = ctx.Manager()
     result = manager.dict()
     port = _free_port()
-    procs = [ctx.Process(target=_worker_lines, args=(r, world, port, lines, cfg, result))
+    procs = [ctx.Process(target=_worker_stream, args=(r, world, port, lines, cfg, result))
              for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(timeout=180)
         assert p.exitcode == 0
-    return [result[r] for r in range(world)]
+    return [result[r] for r in range(world)], dict(result)
+
+
+def _solo(lines):
+    v = mf.Vocabulary(fx.fixture_vocab_lines())
+    recs = [r.field_values(mf.Kind.COMET) for r in mf.records_from_tsv_lines(lines, mf.Kind.COMET)]
+    return score_sharded(fake_score, v, "comet", recs, 128,
+                         mf.BatchConfig(mini_batch=16, maxi_batch_factor=4), 0, 1).tolist()
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_sharded_tokenisation_equals_single_process(world):
-    """score_sharded_lines (each rank encodes 1/w of the lines for the plan, then
-    only its own mini-batches) == score_sharded over the whole encoding."""
+def test_streamed_ranks_equal_single_process(world):
+    """stream_sharded: rank 0 reads a lazy source in rounds of 2 windows, every
+    rank scores its LPT share, scores come back in input order on every rank."""
     lines = fx.fixture_tsv_lines("comet", 301, seed=5)
-    v = mf.Vocabulary(fx.fixture_vocab_lines())
-    recs = [r.field_values(mf.Kind.COMET) for r in mf.records_from_tsv_lines(lines, mf.Kind.COMET)]
-    solo = score_sharded(fake_score, v, "comet", recs, 128,
-                         mf.BatchConfig(mini_batch=16, maxi_batch_factor=4), 0, 1).tolist()
-    got = _run_ranks(world, lines, {"max_len": 128})
-    assert all(g == solo for g in got)
+    got, res = _run_ranks(world, lines, {"max_len": 128})
+    assert all(g == _solo(lines) for g in got)
 
 
-def test_sharded_tokenisation_errors_match_on_every_rank():
-    lines = fx.fixture_tsv_lines("comet", 200, seed=6)
-    lines[150] = "only\ttwo"
-    got = _run_ranks(2, lines, {"max_len": 128})
-    assert got[0] == got[1] == ("ColumnCountError", 150, 2)
-    # max_len too small: raised at window 0 (no bad line there) on every rank
-    got = _run_ranks(2, lines, {"max_len": 1})
+def test_streamed_intake_is_bounded():
+    """The coordinator reads at most 3 rounds ahead of the scoring (bounded
+    queue), whatever the input size."""
+    lines = fx.fixture_tsv_lines("comet", 2000, seed=8)
+    got, res = _run_ranks(2, lines, {"max_len": 128})
+    assert got[0] == got[1] == _solo(lines)
+    per = res["per_round"]
+    trace = res["trace"]
+    assert len(trace) == -(-2000 // per)
+    # round k scores while k+1 is scattered, k+2 queued and k+3 read by the producer
+    assert all(c <= (k + 4) * per for k, c in enumerate(trace)), (trace, per)
+
+
+def test_streamed_errors_match_on_every_rank():
+    lines = fx.fixture_tsv_lines("comet", 400, seed=6)
+    lines[350] = "only\ttwo"
+    got, _ = _run_ranks(2, lines, {"max_len": 128})
+    assert got[0] == got[1] == ("ColumnCountError", 350, 2)
+    # max_len too small: raised at the first record on every rank
+    got, _ = _run_ranks(2, lines, {"max_len": 1})
     assert got[0] == got[1] and got[0][0] == "ValueError"
+    # a device error on a non-coordinator rank ends the stream everywhere
+    got, _ = _run_ranks(3, lines[:300], {"max_len": 128, "fail_rank": 1})
+    assert got[0] == got[1] == got[2] == ("RuntimeError", "device failure on rank 1")
 
 
-def test_sharded_tokenisation_empty_and_tiny_inputs():
-    assert _run_ranks(2, [], {"max_len": 128}) == [[], []]
-    lines = fx.fixture_tsv_lines("comet", 1, seed=3)  # fewer lines than ranks
-    v = mf.Vocabulary(fx.fixture_vocab_lines())
-    recs = [r.field_values(mf.Kind.COMET) for r in mf.records_from_tsv_lines(lines, mf.Kind.COMET)]
-    solo = score_sharded(fake_score, v, "comet", recs, 128,
-                         mf.BatchConfig(mini_batch=16, maxi_batch_factor=4), 0, 1).tolist()
-    assert _run_ranks(3, lines, {"max_len": 128}) == [solo, solo, solo]
+def test_streamed_empty_and_tiny_inputs():
+    got, _ = _run_ranks(2, [], {"max_len": 128})
+    assert got == [[], []]
+    lines = fx.fixture_tsv_lines("comet", 1, seed=3)  # fewer records than ranks
+    got, _ = _run_ranks(3, lines, {"max_len": 128})
+    assert got == [_solo(lines)] * 3
+
+
+def test_lpt_costs_follow_the_model():
+    from paper_2408_11853_b200.parallel import CostModel
+    c2, c5 = CostModel(1024, 4096, 24), CostModel(2560, 10240, 36)
+    # attention's share of a 500-token sequence grows with L relative to the GEMMs
+    share2 = 500 * 500 * c2.c_attn / c2([500])
+    assert 0 < share2 < 0.2
+    assert c5([10]) / c2([10]) == pytest.approx(c5.c_gemm / c2.c_gemm, rel=1e-3)
