@@ -1,28 +1,41 @@
 """Benchmark: COMET-22 (XLM-R-large-shaped) segment scoring on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--precision fp32]
-    python bench.py --impl reference ...      # the reference algorithm on host cores
+    python bench.py --impl reference ...      # the reference itself on the host cores
 
-One step = one maxi-batch window of 1024 records (mini_batch 128 x factor 8,
-the reference Evaluator's default window, `pkg/src/metricforge/evaluate.py:168-177`)
-of synthetic wmt22-comet-da-shaped triplets (content length
-~U{1..126} per field, one id per word, N(0, 0.02^2) random-init weights).
+Workload (strong scaling): ONE shared set of K x records_per_step synthetic
+records of the config (default config 2 = wmt22-comet-da-shaped triplets,
+SURVEY.md §8(d): content length ~U{1..126} per field, one id per word,
+N(0, 0.02^2) random-init weights; K = 20 -> the north star's 100k segments).
+Every rank builds the same set and the reference plan of it (bit-exact
+per-window length sort, `pkg/src/metricforge/batching.py:61-73`); whole
+mini-batches go to ranks longest-processing-time first
+(`paper_2408_11853_b200/parallel.py`), and each rank's share is cut into K
+steps of whole mini-batches. N = 1 scores the whole set.
 
-  value   records/s over K steps with the packed token ids already resident in
-          HBM (mfg_score_device), CUDA events on the stream libmfgpu launches on,
-          max over ranks.
-  e2e     the same metric through the public API: Evaluator.evaluate_lines on
-          host TSV text (tokenisation, plan, packing, H2D, device, D2H, order
-          restore), wall clock with device syncs, max over ranks.
-  roofline  dominant kernel class (a tcgen05 GEMM) from per-launch CUDA events
-          in the timed region: algorithmic FLOPs per launch / mean duration vs
-          the measured sustained bf16 peak (MEASURED_PEAKS.json).
-  cpu_baseline  the reference algorithm (oracle numpy port) on the host cores,
-          bounded sample of the same workload, rank 0 at N=1 only.
+  value   records/s of the whole set with the packed token ids already resident
+          in HBM (mfg_score_device), CUDA events on the stream libmfgpu launches
+          on, per-launch profiling OFF, max over ranks.
+  e2e     the same set through the public API on host TSV text: Evaluator.
+          evaluate_lines at N = 1, DistributedEvaluator.evaluate_lines at N > 1
+          (rank 0 streams the lines, ranks score their LPT shares, scores come
+          back to rank 0): tokenisation, plan, packing, H2D, device, D2H, order
+          restore; wall clock with device syncs, max over ranks.
+  roofline  dominant kernel class (a tcgen05 GEMM) from a separate profiled pass
+          over 2 steps (per-launch CUDA events): algorithmic FLOPs per launch /
+          mean duration vs the measured sustained bf16 peak; `traffic` from the
+          committed ncu capture of the SAME config and precision, else null.
+  parity  the set's config scored against the REFERENCE's own scores
+          (tests/golden/fullsize_cfg<N>.json: 512 / 64 length-stratified records
+          scored by the unmodified metricforge Evaluator; config 1: its 1000
+          scores in reference_vectors.json), every device precision.
+  cpu_baseline  the reference Evaluator itself (baseline/_ref, default
+          BatchConfig) on the host cores, bounded sample, rank 0 at N = 1;
+          the oracle numpy port only when the reference is not installed.
 
-Multi-GPU (torchrun): one rank per GPU, each scores its own windows (records
-are independent; no collective on the data path), barrier + max-over-ranks
-timing; scaling "weak".
+N > 1 without WORLD_SIZE in the environment: the script re-launches itself
+under torchrun (one rank per GPU, NCCL for barriers / max-over-ranks, NCCL
+INFO lines on stderr).
 """
 
 from __future__ import annotations
@@ -31,6 +44,8 @@ import argparse
 import json
 import math
 import os
+import platform
+import socket
 import statistics
 import subprocess
 import sys
@@ -44,8 +59,12 @@ sys.path.insert(0, ROOT)
 
 METRIC = "COMET-22 segments/sec at 1/2/4/8 B200; GEMM tensor-pipe util vs peak"
 UNIT = "segments/s"
-RECORDS_PER_STEP = 1024
+RECORDS_PER_STEP = 5000
 BENCH_DIR = os.environ.get("MFG_BENCH_DIR", "/tmp/mfg_bench")
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+# bounded CPU samples (records): ~10-30 s of reference work on the host cores
+CPU_SAMPLE = {1: 1000, 2: 8, 3: 12, 4: 8, 5: 4}
+REF_PER_STEP = {1: 40, 2: 2, 3: 3, 4: 2, 5: 1}
 
 
 def env_int(k, d):
@@ -138,20 +157,27 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
-def ncu_traffic(cls=None):
-    """dram bytes per launch of kernel class `cls` (else the dominant GEMM) from the
-    newest committed ncu summary (profiles/ncu_summary_*.json)."""
-    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True) \
-            if os.path.isdir(os.path.join(ROOT, "profiles")) else []:
-        if name.startswith("ncu_summary") and name.endswith(".json"):
-            try:
-                with open(os.path.join(ROOT, "profiles", name)) as f:
-                    summ = json.load(f)
-                if cls and cls in summ.get("by_class", {}):
-                    return summ["by_class"][cls]["dram_bytes"], name
-                return summ.get("dram_bytes_per_launch"), name
-            except Exception:
-                pass
+def ncu_traffic(cfg, precision, cls):
+    """DRAM bytes per launch of kernel class `cls` from the newest committed ncu
+    summary captured on THIS config and precision (profiles/ncu_summary_*.json
+    with matching "config" / "precision"); (None, None) when there is none."""
+    pdir = os.path.join(ROOT, "profiles")
+    if not os.path.isdir(pdir):
+        return None, None
+    for name in sorted(os.listdir(pdir), reverse=True):
+        if not (name.startswith("ncu_summary") and name.endswith(".json")):
+            continue
+        try:
+            with open(os.path.join(pdir, name)) as f:
+                summ = json.load(f)
+        except Exception:
+            continue
+        if summ.get("config") != cfg or summ.get("precision") != precision:
+            continue
+        entry = summ.get("by_class", {}).get(cls)
+        if entry:
+            return entry["dram_bytes"], {"file": name,
+                                         "tokens_per_launch": summ.get("tokens_per_launch")}
     return None, None
 
 
@@ -162,98 +188,175 @@ def workload_lines(cfg, n, seed):
     return fx.synthetic_tsv_lines(cfg, n, seed=seed)
 
 
-def oracle_model(cfg):
-    from oracle import fixtures as fx
-    from oracle import tokenizer as otk
-    from oracle.encoder import OracleModel
-    man = dict(fx.CONFIGS[cfg])
-    if cfg == 1:
-        return OracleModel(man, fx.fixture_weights(man, 1234)), otk.OracleVocab(fx.fixture_vocab_lines())
-    return (OracleModel(man, dict(fx.synthetic_weights(man))),
-            otk.OracleVocab(fx.synthetic_vocab_lines(man["vocab_size"])))
+def cpu_info():
+    model = platform.processor() or platform.machine()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        avail = len(os.sched_getaffinity(0))
+    except AttributeError:
+        avail = os.cpu_count()
+    return {"cpu": model, "cpu_count": os.cpu_count(), "affinity": avail}
 
 
-def cpu_baseline(cfg, n_records, return_scores=False):
-    """Reference algorithm (oracle numpy port) on host cores, bounded sample."""
-    from oracle import evaluate as oe
-    from oracle import fixtures as fx
-    from oracle import tokenizer as otk
-    from oracle.encoder import OracleModel
-
-    model, vocab = oracle_model(cfg)
-    lines = workload_lines(cfg, n_records, fx.TEXT_SEED + 777)
-    oe.score_lines(model, vocab, lines[:1])  # discard run (BLAS warmup)
-    t0 = time.perf_counter()
-    ref_scores, _ = oe.score_lines(model, vocab, lines)
-    dt = time.perf_counter() - t0
+def blas_threads():
     try:
         from threadpoolctl import threadpool_info
-        cores = max((p.get("num_threads", 1) for p in threadpool_info()), default=1)
+        return max((p.get("num_threads", 1) for p in threadpool_info()
+                    if p.get("user_api") == "blas"), default=1)
     except Exception:
-        cores = os.cpu_count() or 1
-    out = {"value": n_records / dt, "unit": UNIT, "cores": int(cores), "kind": "port",
-           "sample": f"{n_records} synthetic config-{cfg} records (oracle numpy port of "
-                     f"pkg/src/metricforge/encoder.py, fp32, {dt:.1f} s)"}
-    return (out, lines, ref_scores) if return_scores else out
+        return os.cpu_count() or 1
 
 
-def parity_report(path, vocab_path, lines, ref, device, cfg_id):
-    """Same records through the device path at every precision vs the fp32
-    oracle (the reference algorithm): max/mean |delta| and Pearson; the fp16
-    mode also against the oracle's fp16 mode (the reference's binary16 path)."""
+def reference_available():
+    return os.path.isfile(os.path.join(REF_DIR, "metricforge", "__init__.py"))
+
+
+def import_reference():
+    """The unmodified reference package installed in baseline/_ref."""
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import metricforge
+    return metricforge
+
+
+class CpuReference:
+    """The reference's own CPU path for a config: `metricforge.Evaluator`
+    (default BatchConfig, fp32, validate=False) from baseline/_ref, or — only
+    when it is not installed — the oracle numpy port of the same algorithm."""
+
+    def __init__(self, cfg, path, vocab):
+        self.cfg = cfg
+        if reference_available():
+            ref = import_reference()
+            self.kind = "reference"
+            self.ev = ref.Evaluator(ref.EvaluatorConfig(model=path, vocab=vocab, quiet=True,
+                                                        validate=False))
+            self.what = ("metricforge.Evaluator (baseline/_ref, pkg/src/metricforge/"
+                         "evaluate.py:126-241), default BatchConfig, fp32")
+        else:
+            from oracle import fixtures as fx
+            from oracle import tokenizer as otk
+            from oracle.encoder import OracleModel
+            man = dict(fx.CONFIGS[cfg])
+            w = fx.fixture_weights(man, 1234) if cfg == 1 else dict(fx.synthetic_weights(man))
+            vl = fx.fixture_vocab_lines() if cfg == 1 else fx.synthetic_vocab_lines(man["vocab_size"])
+            self.kind = "port"
+            self.model, self.vocab = OracleModel(man, w), otk.OracleVocab(vl)
+            self.what = "oracle numpy port of pkg/src/metricforge/encoder.py (reference not installed)"
+
+    def score(self, lines):
+        if self.kind == "reference":
+            return list(self.ev.evaluate_lines(lines).segment_scores)
+        from oracle import evaluate as oe
+        return oe.score_lines(self.model, self.vocab, lines)[0]
+
+    def describe(self, value, sample):
+        return {"value": value, "unit": UNIT, "cores": blas_threads(), "kind": self.kind,
+                "workers": 1, "sample": sample, "implementation": self.what, **cpu_info()}
+
+
+def cpu_baseline(cfg, path, vocab, n_records):
+    """Bounded sample of the config's workload through the reference on the
+    host cores (1 discarded record, then the sample once, like the reference
+    bench's discard + timed passes, `cli.py:309-315`)."""
+    from oracle import fixtures as fx
+    ref = CpuReference(cfg, path, vocab)
+    lines = workload_lines(cfg, n_records + 1, fx.TEXT_SEED + 777)
+    ref.score(lines[:1])
+    t0 = time.perf_counter()
+    ref.score(lines[1:])
+    dt = time.perf_counter() - t0
+    return ref.describe(n_records / dt, f"{n_records} synthetic config-{cfg} records scored in "
+                                       f"{dt:.1f} s (one mini-batch of the default BatchConfig; "
+                                       f"BLAS threads = cores)")
+
+
+def load_fullsize_golden(cfg):
+    p = os.path.join(ROOT, "tests", "golden", f"fullsize_cfg{cfg}.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f)
+
+
+def parity_report(cfg, path, vocab_path, device):
+    """The config's parity set through the device path at every precision
+    against the REFERENCE's own scores (fp32; the fp16 mode also against the
+    reference's fp16 mode): n, max / mean |delta|, Pearson."""
     import paper_2408_11853_b200 as mf
-    from oracle import evaluate as oe
-    from oracle.encoder import OracleModel
+    from oracle import fixtures as fx
 
-    ref = np.asarray(ref, dtype=np.float64)
-    out = {"n_records": len(lines), "tolerance": 1e-3, "reference": "oracle fp32 (numpy port)"}
+    if cfg == 1:
+        with open(os.path.join(ROOT, "tests", "golden", "reference_vectors.json")) as f:
+            g1 = json.load(f)["config1"]
+        lines = fx.fixture_tsv_lines("comet", len(g1["scores"]), seed=0)
+        ref = {"fp32": g1["scores"]}
+        src = "reference Evaluator scores (tests/golden/reference_vectors.json config1)"
+    else:
+        g = load_fullsize_golden(cfg)
+        if g is None:
+            return {"unavailable": f"tests/golden/fullsize_cfg{cfg}.json not generated"}
+        if mf.read_manifest(path).checksum != g["checksum"]:
+            return {"unavailable": "regenerated container checksum differs from the golden's"}
+        _, lines = fx.parity_subset(cfg, g["n"], g["pool"], g["text_seed"])
+        ref = {k: g[k] for k in ("fp32", "fp16") if k in g}
+        src = (f"reference Evaluator scores (tests/golden/fullsize_cfg{cfg}.json, "
+               f"{g['n']} length-stratified records)")
+    out = {"n_records": len(lines), "tolerance": 1e-3, "reference": src}
 
     def stats(got, want):
+        got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
         d = np.abs(got - want)
         pear = float(np.corrcoef(got, want)[0, 1]) if len(got) > 2 and want.std() > 0 else None
         return {"max_abs": float(d.max()), "mean_abs": float(d.mean()), "pearson": pear}
 
     for prec in ("fp32", "bf16x3", "bf16", "fp16"):
-        cfg = mf.EvaluatorConfig(model=path, vocab=vocab_path, quiet=True, validate=False,
-                                 device=device, precision=prec)
-        with mf.Evaluator(cfg) as ev:
-            got = np.asarray(ev.evaluate_lines(lines).segment_scores, dtype=np.float64)
-        out[prec] = stats(got, ref)
-        if prec == "fp16":
-            model32, vocab = oracle_model(cfg_id)
-            m16 = OracleModel(model32.m, {k: v for k, v in model32.w.items()}, mode="fp16")
-            want16, _ = oe.score_lines(m16, vocab, lines)
-            out["fp16"]["vs_reference_fp16_mode"] = stats(got, np.asarray(want16, np.float64))
+        c = mf.EvaluatorConfig(model=path, vocab=vocab_path, quiet=True, validate=False,
+                               device=device, precision=prec)
+        with mf.Evaluator(c) as ev:
+            got = ev.evaluate_lines(lines).segment_scores
+            fb = ev.model.stats()["fallback_chunks"]
+        out[prec] = stats(got, ref["fp32"])
+        if fb:
+            out[prec]["fallback_chunks"] = fb
+        if prec == "fp16" and "fp16" in ref:
+            out["fp16"]["vs_reference_fp16_mode"] = stats(got, ref["fp16"])
     out["fp32_within_tolerance"] = out["fp32"]["max_abs"] <= 1e-3
     return out
 
 
 # --------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
+    """The reference's own CPU implementation on the box's host cores, same
+    metric / unit / config as our arm; each step a bounded sample."""
     if rank != 0:
         return
-    per_step = 2 if args.config >= 2 else 64
-    base = cpu_baseline(args.config, per_step)  # also warms BLAS
-    from oracle import evaluate as oe
     from oracle import fixtures as fx
-    from oracle import tokenizer as otk
-    from oracle.encoder import OracleModel
-
-    model, vocab = oracle_model(args.config)
-    lines = workload_lines(args.config, per_step * (args.steps + args.warmup), fx.TEXT_SEED)
-    chunks = [lines[i * per_step:(i + 1) * per_step] for i in range(args.steps + args.warmup)]
+    man, path, vocab = prepare_model(args.config, 0, 1, lambda: None)
+    ref = CpuReference(args.config, path, vocab)
+    per_step = REF_PER_STEP[args.config]
+    n_steps = args.steps + args.warmup
+    lines = workload_lines(args.config, per_step * n_steps, fx.TEXT_SEED)
+    chunks = [lines[i * per_step:(i + 1) * per_step] for i in range(n_steps)]
     for c in chunks[:args.warmup]:
-        oe.score_lines(model, vocab, c)
+        ref.score(c)
     t0 = time.perf_counter()
     for c in chunks[args.warmup:]:
-        oe.score_lines(model, vocab, c)
+        ref.score(c)
     dt = time.perf_counter() - t0
     value = per_step * args.steps / dt
-    base.update(value=value, sample=f"{per_step} records per step x {args.steps} steps (oracle "
-                                    f"numpy port of the reference encoder, fp32)")
+    base = ref.describe(value, f"{per_step} records per step x {args.steps} steps "
+                               f"(bounded sample of the config-{args.config} workload)")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": f"config {args.config}: " + fx.CONFIG_NAMES[args.config],
                        "records_per_step": per_step},
@@ -263,64 +366,107 @@ def run_reference(args, rank, world):
 
 
 # --------------------------------------------------------------------------- our arm
+def rank_steps(seq_off, n_seq, n_records, batch_cfg, world, rank, n_steps, cost):
+    """The reference plan of the whole set, whole mini-batches LPT-assigned to
+    ranks, this rank's share cut into `n_steps` runs of whole mini-batches of
+    about equal cost. Returns (order, per-step arrays of plan positions)."""
+    from paper_2408_11853_b200.parallel import shard_plan
+    order, batches, assign = shard_plan(seq_off, n_seq, n_records, batch_cfg, world, cost)
+    mine = assign[rank]
+    lens = np.diff(seq_off).reshape(n_records, n_seq)
+    costs = np.array([cost(lens[order[a:b]].ravel()) for a, b in (batches[i] for i in mine)])
+    cum = np.cumsum(costs)
+    total = cum[-1] if len(cum) else 0.0
+    steps, start = [], 0
+    for s in range(n_steps):
+        stop = int(np.searchsorted(cum, total * (s + 1) / n_steps, side="left")) + 1 \
+            if s + 1 < n_steps else len(mine)
+        stop = max(start, min(stop, len(mine)))
+        sel = mine[start:stop]
+        steps.append(np.concatenate([np.arange(*batches[b]) for b in sel]) if sel
+                     else np.zeros(0, np.int64))
+        start = stop
+    return order, steps
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
     import paper_2408_11853_b200 as mf
     from oracle import fixtures as fx
-    from paper_2408_11853_b200.batching import pack_roles, plan_order
+    from paper_2408_11853_b200.batching import pack_roles
+    from paper_2408_11853_b200.parallel import CostModel, DistributedEvaluator
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    gloo = dist.is_initialized() and dist.get_backend() == "gloo"
+    red_dev = "cpu" if gloo else dev
 
     def barrier():
         if world > 1:
             dist.barrier()
 
+    def max_over_ranks(*vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=red_dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(v) for v in t.tolist()]
+
     man, path, vocab_path = prepare_model(args.config, rank, world, barrier)
-    n_steps = args.steps + args.warmup
-    R = args.records_per_step
-    lines = workload_lines(args.config, R * n_steps, fx.TEXT_SEED + 1000 * rank)
+    K, R = args.steps, args.records_per_step
+    G = K * R                                    # the shared set (strong scaling)
+    t_gen = time.perf_counter()
+    lines = workload_lines(args.config, G, fx.TEXT_SEED)
+    gen_s = time.perf_counter() - t_gen
+    kind = mf.Kind.parse(man["like"])
+    ns = mf.kinds.N_SEQUENCES[kind]
+    max_len = min(512, man["max_position"])
+    vocab = mf.load_vocab(vocab_path)
+    batch_cfg = mf.BatchConfig()
+    cost = CostModel(man["d_model"], man["d_ffn"], man["n_layers"])
 
     # ---------------- device-resident timing (value)
+    ids, off = vocab.encode_tsv(kind, lines, max_len)
+    total_tokens = int(off[-1])
+    order, step_pos = rank_steps(off, ns, G, batch_cfg, world, rank, K, cost)
+    steps = []
+    for pos in step_pos:
+        if len(pos):
+            packed, cu = pack_roles(ids, off, ns, order[pos])
+            steps.append((torch.from_numpy(packed).to(dev), cu, len(pos)))
+        else:
+            steps.append((None, np.zeros(1, np.int64), 0))
+    my_records = sum(s[2] for s in steps)
+    my_tokens = sum(int(s[1][-1]) for s in steps)
+    del ids
     t_load = time.perf_counter()
-    model = mf.GpuScoringModel(path, device=local_rank, precision=args.precision,
-                               profile=True)
+    model = mf.GpuScoringModel(path, device=local_rank, precision=args.precision, profile=False)
     torch.cuda.synchronize()
     load_s = time.perf_counter() - t_load
-    vocab = mf.load_vocab(vocab_path)
-    kind = mf.Kind.parse(man["like"])
-    max_len = min(512, man["max_position"])
-    n_seq = mf.kinds.N_SEQUENCES[kind]
-    steps = []
-    tokens_per_step = []
-    for s in range(n_steps):
-        chunk = lines[s * R:(s + 1) * R]
-        recs = list(mf.records_from_tsv_lines(chunk, kind))
-        ids, off = vocab.encode_batch(kind, [r.field_values(kind) for r in recs], max_len)
-        lengths = np.diff(off).reshape(R, n_seq).sum(1)
-        order = plan_order(lengths, mf.BatchConfig())
-        packed, cu = pack_roles(ids, off, n_seq, order)
-        steps.append((torch.from_numpy(packed).to(dev), cu))
-        tokens_per_step.append(int(cu[-1]))
-    out = torch.empty(R, dtype=torch.float32, device=dev)
+    out = torch.empty(max(1, max(s[2] for s in steps)), dtype=torch.float32, device=dev)
     stream = torch.cuda.Stream(device=dev)
     model.set_stream(stream.cuda_stream)
+
+    def run_step(m, s):
+        t, cu, n = steps[s]
+        if n:
+            m.score_device(t.data_ptr(), cu, n, out.data_ptr())
+
     for s in range(args.warmup):
-        model.score_device(steps[s][0].data_ptr(), steps[s][1], R, out.data_ptr())
-    torch.cuda.synchronize()
-    model.reset_stats()
-    barrier()
+        run_step(model, s % K)
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
 
     def timed_region():
+        model.reset_stats()
+        barrier()
+        torch.cuda.synchronize()
         with ClockSampler(local_rank) as c:
             ev0.record(stream)
-            for s in range(args.warmup, n_steps):
-                model.score_device(steps[s][0].data_ptr(), steps[s][1], R, out.data_ptr())
+            for s in range(K):
+                run_step(model, s)
             ev1.record(stream)
             torch.cuda.synchronize()
         barrier()
@@ -330,15 +476,20 @@ def run_ours(args, rank, world, local_rank):
     # a run that saw hardware / thermal slowdown is re-measured once (decided
     # jointly so every rank runs the same number of timed regions)
     bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
-    flag = torch.tensor([1.0 if bad & set(clk.summary()["reasons"]) else 0.0],
-                        device="cpu" if dist.is_initialized() and dist.get_backend() == "gloo" else dev)
-    if world > 1:
-        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
-    remeasured = bool(flag.item())
+    remeasured = max_over_ranks(1.0 if bad & set(clk.summary()["reasons"]) else 0.0)[0] > 0
     if remeasured:
-        model.reset_stats()
         ms, clk = timed_region()
-    stats = model.stats()
+    launches = int(model.stats()["kernel_launches"])
+
+    # ---------------- per-launch class times: a separate profiled pass (2 steps)
+    model.set_profile(True)
+    model.reset_stats()
+    for s in range(min(2, K)):
+        run_step(model, s)
+    torch.cuda.synchronize()
+    model.set_profile(False)
+    pstats = model.stats()
+    load_phases = model.load_phases()
     model.set_stream(0)
     model.close()
 
@@ -350,52 +501,49 @@ def run_ours(args, rank, world, local_rank):
                 continue
             m2 = mf.GpuScoringModel(path, device=local_rank, precision=prec)
             m2.set_stream(stream.cuda_stream)
-            for s in range(min(args.warmup, 2)):
-                m2.score_device(steps[s][0].data_ptr(), steps[s][1], R, out.data_ptr())
-            k2 = min(args.steps, 6)
+            run_step(m2, 0)
+            k2 = min(K, 6)
             torch.cuda.synchronize()
             ev0.record(stream)
-            for s in range(args.warmup, args.warmup + k2):
-                m2.score_device(steps[s][0].data_ptr(), steps[s][1], R, out.data_ptr())
+            for s in range(k2):
+                run_step(m2, s)
             ev1.record(stream)
             torch.cuda.synchronize()
             ms2 = ev0.elapsed_time(ev1)
+            n2 = sum(steps[s][2] for s in range(k2))
             m2.set_stream(0)
             m2.close()
-            others[prec] = {"value": R * k2 / (ms2 / 1000.0), "unit": UNIT, "steps": k2,
+            others[prec] = {"value": n2 / (ms2 / 1000.0), "unit": UNIT, "steps": k2,
                             "ms_per_step": ms2 / k2}
     del steps
+    torch.cuda.empty_cache()
 
     # ---------------- end to end through the public API (e2e)
     cfg = mf.EvaluatorConfig(model=path, vocab=vocab_path, quiet=True, validate=False,
                              device=local_rank, precision=args.precision)
-    with mf.Evaluator(cfg) as ev:
-        ev.evaluate_lines(lines[:R * args.warmup])
+    ev = DistributedEvaluator(cfg) if world > 1 else mf.Evaluator(cfg)
+    with ev:
+        warm = lines[:min(G, 2 * batch_cfg.window * max(1, world))]
+        ev.evaluate_lines(warm if rank == 0 else None) if world > 1 else ev.evaluate_lines(warm)
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        rep = ev.evaluate_lines(lines[R * args.warmup:])
+        rep = ev.evaluate_lines(lines if rank == 0 or world == 1 else None)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
-        e2e_stats = ev.model.stats()
     barrier()
-    assert len(rep.segment_scores) == R * args.steps
+    assert len(rep.segment_scores) == G
     assert all(math.isfinite(v) for v in rep.segment_scores)
 
     # ---------------- reduce over ranks
-    vals = torch.tensor([ms, e2e_s], dtype=torch.float64,
-                        device="cpu" if dist.is_initialized() and dist.get_backend() == "gloo" else dev)
-    if world > 1:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    ms_max, e2e_max = float(vals[0]), float(vals[1])
+    ms_max, e2e_max = max_over_ranks(ms, e2e_s)
     if rank != 0:
         return
-    total = R * args.steps * world
-    value = total / (ms_max / 1000.0)
-    e2e_value = total / e2e_max
+    value = G / (ms_max / 1000.0)
+    e2e_value = G / e2e_max
 
     peaks, peak_src = measured_peaks()
-    cls = stats["classes"]
+    cls = pstats["classes"]
     gemm_names = ("qkv", "o_proj", "ffn1", "ffn2")
     dom = max(gemm_names, key=lambda k: cls[k]["ms"])
     c = cls[dom]
@@ -403,26 +551,29 @@ def run_ours(args, rank, world, local_rank):
     achieved = (c["flops"] / max(1, c["launches"])) / (per_launch_ms / 1e3) / 1e12
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
     mma_per_step = 1 if args.precision in ("bf16", "fp16") else 3
-    traffic, traffic_src = ncu_traffic(dom)
+    traffic, traffic_src = ncu_traffic(args.config, args.precision, dom)
     gemm_ms = sum(cls[k]["ms"] for k in gemm_names)
     gemm_flops = sum(cls[k]["flops"] for k in gemm_names)
     all_ms = sum(v["ms"] for v in cls.values())
     roofline = {
-        "bound": "tensor", "kernel": f"gemm_tc_kernel ({dom})", "achieved": achieved,
+        "bound": "tensor", "kernel": f"gemm2_tc_kernel ({dom})", "achieved": achieved,
         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
         "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
         "algorithmic_flops_per_launch": c["flops"] / max(1, c["launches"]),
         "mean_launch_ms": per_launch_ms,
+        "tokens_per_launch": pstats["tokens"] / max(1, pstats["chunks"]),
         "issued_mma_per_algorithmic": mma_per_step,
         "issued_frac": achieved * mma_per_step / peak,
         "all_gemms": {"achieved_tflops": gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else None,
                       "share_of_step": gemm_ms / all_ms if all_ms else None},
         "class_ms_share": {k: v["ms"] / all_ms for k, v in cls.items()} if all_ms else {},
+        "timing": "class times from a separate profiled pass over 2 steps (per-launch CUDA "
+                  "events on libmfgpu's stream); the timed region ran with profiling off",
         "traffic_source": traffic_src,
     }
     if cls["attention"]["ms"]:
         gbs = cls["attention"]["bytes"] / (cls["attention"]["ms"] / 1e3) / 1e9
-        att_traffic, _ = ncu_traffic("attention")
+        att_traffic, _ = ncu_traffic(args.config, args.precision, "attention")
         roofline["attention_hbm"] = {
             "achieved_gbs": gbs, "peak_gbs": peaks.get("hbm_gbs"),
             "frac": gbs / peaks.get("hbm_gbs", 6544.3),
@@ -433,12 +584,15 @@ def run_ours(args, rank, world, local_rank):
         gbs = cls["layernorm"]["bytes"] / (cls["layernorm"]["ms"] / 1e3) / 1e9
         roofline["layernorm_hbm"] = {"achieved_gbs": gbs, "peak_gbs": peaks.get("hbm_gbs"),
                                      "frac": gbs / peaks.get("hbm_gbs", 6544.3)}
-    h2d = sum(tokens_per_step[args.warmup:]) * 4 / args.steps + (3 * R + 1) * 4 + 8 * (
-        sum(tokens_per_step[args.warmup:]) / args.steps / 64 + 3 * R)
+    # host<->device bytes of the e2e path per step: int32 token ids, int64
+    # cu_seqlens and the attention tile plan (8 B per 64 tokens + 8 B per
+    # sequence) in; float32 scores out
+    n_seqs = G * ns
+    h2d = total_tokens * 4 + (n_seqs + 1) * 8 + 8 * (total_tokens / 64 + n_seqs)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
         "dtype": {"fp32": "fp16x3-split (fp32-parity)", "bf16x3": "bf16x3-split",
                   "bf16": "bf16", "fp16": "fp16 (reference binary16 mode)"}[args.precision],
         "data": ("synthetic (reference fixture generator, std-0.25 fixture weights)" if args.config == 1
@@ -446,27 +600,55 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": f"config {args.config}: " + fx.CONFIG_NAMES[args.config],
                    "model": "XLM-R-large-shaped encoder (24 x d1024 x h16 x ffn4096) + "
                             "head [6144,3072,1024,1]" if args.config == 2 else fx.CONFIG_NAMES[args.config],
-                   "records_per_step": R, "tokens_per_step": sum(tokens_per_step[args.warmup:]) / args.steps,
-                   "precision": args.precision, "parallelism": f"dp{world} (records sharded)",
+                   "global_records": G, "records_per_step": R,
+                   "tokens": total_tokens, "records_rank0": my_records, "tokens_rank0": my_tokens,
+                   "precision": args.precision,
+                   "parallelism": f"dp{world} (whole mini-batches LPT-sharded over ranks, "
+                                  "no data-path collective)",
                    "l2": "inputs larger than L2 ({:.1f} GB of layer weights + GB-scale activations "
                          "per step)".format(man["n_layers"] * (4 * man["d_model"] ** 2 + 2 * man["d_model"]
                                                                * man["d_ffn"]) *
                                             (4 if args.precision in ("fp32", "bf16x3") else 2) / 1e9)},
         "roofline": roofline,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": R * 4 + 4,
-                "path": "Evaluator.evaluate_lines (host TSV -> libmfhost -> libmfgpu -> scores)"},
-        "gpu_launches": int(stats["kernel_launches"]),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d / K),
+                "d2h_bytes_per_step": int(G * 4 / K),
+                "path": ("DistributedEvaluator.evaluate_lines (rank 0 streams host TSV; per rank "
+                         "libmfhost -> libmfgpu; scores gathered on rank 0)" if world > 1 else
+                         "Evaluator.evaluate_lines (host TSV -> libmfhost -> libmfgpu -> scores)")},
+        "gpu_launches": launches,
         "other_precisions": others,
         "model_load_s": load_s,
+        "model_load_phases_ms": load_phases,
+        "workload_generation_s": gen_s,
         "clocks": dict(clk.summary(), remeasured=remeasured),
     }
     if world == 1 and not args.no_cpu_baseline:
-        n_cpu = args.cpu_records or {1: 1024, 5: 4}.get(args.config, 8)
-        base, ref_lines, ref = cpu_baseline(args.config, n_cpu, return_scores=True)
-        line["cpu_baseline"] = base
-        line["parity"] = parity_report(path, vocab_path, ref_lines, ref, local_rank, args.config)
+        n_cpu = args.cpu_records or CPU_SAMPLE[args.config]
+        line["cpu_baseline"] = cpu_baseline(args.config, path, vocab_path, n_cpu)
+        g = load_fullsize_golden(args.config)
+        if g and "seconds" in g:
+            line["cpu_baseline"]["large_sample_dev_container"] = {
+                "records": g["n"], "seconds": g["seconds"], "host": g.get("host"),
+                "note": "the same reference Evaluator on the full parity set, measured when the "
+                        "golden was generated (development container, not this box)"}
+    if world == 1 and not args.no_parity:
+        line["parity"] = parity_report(args.config, path, vocab_path, local_rank)
     print(json.dumps(line), flush=True)
+
+
+def self_launch(args):
+    """`bench.py --gpus N` (N > 1) outside torchrun: one rank per GPU."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # keep stdout = the JSON line
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -477,11 +659,12 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16x3", "bf16", "fp16"])
-    ap.add_argument("--records-per-step", type=int, default=RECORDS_PER_STEP)
+    ap.add_argument("--records-per-step", type=int, default=RECORDS_PER_STEP,
+                    help="global records per step; the shared set is steps x this")
     ap.add_argument("--cpu-records", type=int, default=None,
-                    help="CPU-baseline / parity sample (default: 1024 at config 1, 4 at config 5, "
-                         "else 8 records: ~5-30 s of host work)")
+                    help="CPU-baseline sample (default ~10-30 s of reference work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-other-precisions", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -489,7 +672,9 @@ def main():
     local_rank = env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         run_reference(args, rank, world)
-        return
+        return 0
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     # MFG_BENCH_BACKEND=gloo: code-path check of the multi-rank bench on a box with
     # fewer GPUs than ranks (ranks share devices; not a measurement)
     backend = os.environ.get("MFG_BENCH_BACKEND", "nccl")
@@ -497,7 +682,7 @@ def main():
         import torch
         import torch.distributed as dist
         if backend == "gloo":
-            local_rank %= torch.cuda.device_count()
+            local_rank %= max(1, torch.cuda.device_count())
             dist.init_process_group("gloo")
         else:
             torch.cuda.set_device(local_rank)
@@ -508,7 +693,8 @@ def main():
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

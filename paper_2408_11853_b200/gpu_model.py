@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import functools
 import os
 import threading
 
@@ -42,6 +43,9 @@ class ComputeMode(enum.Enum):
     def parse(cls, value):
         if isinstance(value, cls):
             return value
+        # the reference's own ComputeMode (metricforge.encoder) when the
+        # reference Evaluator constructs this model through its seam
+        value = getattr(value, "value", value)
         try:
             return cls(value)
         except ValueError:
@@ -65,10 +69,64 @@ def _device_ordinal(device) -> int:
     return int(s)
 
 
+# feature width per kind, in units of d_model (`encoder.py:198-212`)
+FEATURE_WIDTH = {Kind.COMET_QE: 4, Kind.COMET: 6, Kind.BLEURT: 1}
+
+
+def required_tensor_shapes(manifest) -> dict:
+    """Tensor name -> shape contract of a manifest, the one `mfg_create`
+    enforces natively (`csrc/container.hpp`); same names and shapes as the
+    reference's `required_tensor_shapes` (`encoder.py:69-91`)."""
+    d, f = int(manifest.d_model), int(manifest.d_ffn)
+    out = {"emb.tok": (int(manifest.vocab_size), d), "emb.pos": (int(manifest.max_position), d)}
+    layer = {f"att.{p}.{t}": ((d, d) if t == "w" else (d,)) for p in "qkvo" for t in "wb"}
+    layer.update({f"{n}.{t}": (d,) for n in ("norm1", "norm2") for t in "gb"})
+    layer.update({"ffn.w1": (d, f), "ffn.b1": (f,), "ffn.w2": (f, d), "ffn.b2": (d,)})
+    for i in range(int(manifest.n_layers)):
+        out.update({f"layer.{i}.{k}": v for k, v in layer.items()})
+    widths = [FEATURE_WIDTH[Kind.parse(manifest.like)] * d, *map(int, manifest.head_hidden), 1]
+    for j, (a, b) in enumerate(zip(widths, widths[1:])):
+        out[f"head.{j}.w"], out[f"head.{j}.b"] = (a, b), (b,)
+    return out
+
+
+@functools.lru_cache(maxsize=None)
+def _reference_errors():
+    import importlib
+    ref = importlib.import_module("metricforge.errors")
+
+    class ReferenceDeviceError(DeviceError, ref.MetricForgeError):
+        """DeviceError that is also the reference's MetricForgeError."""
+
+    return ref.ContainerError, ReferenceDeviceError
+
+
+def _error_classes(container):
+    """(ContainerError, DeviceError) to raise. When the caller is the reference
+    itself (its `Evaluator` constructs the model at `evaluate.py:151` with a
+    `metricforge.container.ModelContainer`), container errors are the
+    reference's own `metricforge.errors.ContainerError` so its callers'
+    `except` clauses still match (`encoder.py:108-115`)."""
+    mod = type(container).__module__ or ""
+    if mod.split(".")[0] == "metricforge":
+        return _reference_errors()
+    return ContainerError, DeviceError
+
+
 class GpuScoringModel:
+    """Drop-in for the reference `ScoringModel` at its seam: the constructor
+    takes `(container, compute_mode)` (the reference's own container and
+    ComputeMode objects, or a path / this package's), and `score_records`
+    keeps the contract the reference `Evaluator` relies on
+    (`evaluate.py:151, 166, 173-175`). The padded-batch internals `forward`,
+    `pool`, `encode_pooled`, `features` and `head` (`encoder.py:154-212`)
+    are not part of that contract and are not provided: the device path fuses
+    them into one call per batch."""
+
     def __init__(self, container, compute_mode=ComputeMode.FP32, device=None, precision=None,
                  max_tokens=0, max_records=0, profile=False):
         path = container if isinstance(container, (str, os.PathLike)) else container.path
+        self._ContainerError, self._DeviceError = _error_classes(container)
         self.manifest = None if isinstance(container, (str, os.PathLike)) else container.manifest
         self.mode = ComputeMode.parse(compute_mode)
         self.precision = precision or default_precision(self.mode)
@@ -83,7 +141,7 @@ class GpuScoringModel:
         rc = self._lib.mfg_create(C.byref(cfg), C.byref(handle))
         if rc != 0:
             code, msg = native.last_error(None)
-            raise (ContainerError if rc == 3 else ValueError if rc == 2 else DeviceError)(msg)
+            raise self._error(rc, msg)
         self._h = handle
         self._lock = threading.Lock()
         info = native.MfgModelInfo()
@@ -93,6 +151,13 @@ class GpuScoringModel:
         self.n_roles = int(info.n_roles)
         self.max_position = int(info.max_position)
         self.vocab_size = int(info.vocab_size)
+
+    def _error(self, rc, msg):
+        """C-ABI return code -> exception: 2 usage (ValueError, as the
+        reference's id/length checks), 3 container, else device/runtime."""
+        if rc == 2:
+            return ValueError(msg)
+        return (self._ContainerError if rc == 3 else self._DeviceError)(msg)
 
     # ------------------------------------------------------------------ core
     def score_packed(self, ids, cu_seqlens, n_records) -> np.ndarray:
@@ -104,13 +169,13 @@ class GpuScoringModel:
             return out
         with self._lock:
             if self._h is None:
-                raise DeviceError("scoring model is closed")
+                raise self._DeviceError("scoring model is closed")
             rc = self._lib.mfg_score_batch(self._h, int(n_records), self.n_roles,
                                            native.ptr(ids, C.c_int32), native.ptr(cu, C.c_int64),
                                            native.ptr(out, C.c_float))
             if rc != 0:
                 _, msg = native.last_error(self._h)
-                raise (ValueError if rc == 2 else ContainerError if rc == 3 else DeviceError)(msg)
+                raise self._error(rc, msg)
         return out
 
     def score_device(self, ids_ptr, cu_seqlens, n_records, scores_ptr):
@@ -123,7 +188,7 @@ class GpuScoringModel:
                                             C.c_void_p(scores_ptr))
             if rc != 0:
                 _, msg = native.last_error(self._h)
-                raise (ValueError if rc == 2 else ContainerError if rc == 3 else DeviceError)(msg)
+                raise self._error(rc, msg)
 
     def set_stream(self, stream_handle):
         """Route every launch to an external cudaStream_t (int handle; 0 = own)."""

@@ -94,6 +94,7 @@ def test_multi_rank_cli_streams_stdin_like_one_gpu(tiny_factory, tmp_path):
     assert len(one.stdout.splitlines()) == 700 and two.stdout == one.stdout
     cols = [[l.split("\t")[k] for l in lines] for k in range(3)]
     cols[1][3] = "north\twind"  # legal in a field file: only line ends separate records
+    cols[0][5] = "the north"  # field files use splitlines() (cli.py:129): no lone '\r' here
     paths = []
     for k, name in enumerate(("s", "t", "r")):
         p = tmp_path / f"{name}.txt"
