@@ -84,6 +84,14 @@ int mfg_last_error(const mfg_ctx* ctx, int32_t* code, char* buf, size_t cap);
 
 void mfg_destroy(mfg_ctx* ctx);
 
+/* Host-only check of a container (no device needed): mmap + header, tensor
+ * index bounds (offsets / sizes inside the file, no overlaps, no duplicate
+ * names), metric kind and the tensor-name/shape contract — what mfg_create
+ * validates before touching the GPU (`container.py:293-322`,
+ * `encoder.py:107-115`). The payload checksum is the Python
+ * `open_container(validate=True)` step. Error text via mfg_last_error(NULL). */
+int mfg_check_container(const char* path);
+
 /* ---- introspection ------------------------------------------------------ */
 typedef struct {
   int32_t kind; /* 0 comet-qe, 1 comet, 2 bleurt */

@@ -8,6 +8,7 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -190,7 +191,8 @@ class Container {
       base_ = nullptr;
       throw std::runtime_error(path + ": mmap failed");
     }
-    if (memcmp(base_, "MFRG0001", 8) != 0) throw ContainerError(path + ": not a model container (bad magic)");
+    if (size_ < 8 || memcmp(base_, "MFRG0001", 8) != 0)
+      throw ContainerError(path + ": not a model container (bad magic)");
     if (size_ < 12) throw ContainerError(path + ": truncated before header length");
     uint32_t hlen;
     memcpy(&hlen, base_ + 8, 4);
@@ -220,6 +222,7 @@ class Container {
       if ((int64_t)fv->num != 1)
         throw ContainerError(path + ": format_version " + std::to_string((int64_t)fv->num) + " not supported");
     const JVal* ts = h.get("tensors");
+    std::vector<std::pair<int64_t, int64_t>> regions;
     if (ts)
       for (auto& e : ts->arr) {
         TensorView tv;
@@ -229,17 +232,31 @@ class Container {
         tv.dtype = dt->str;
         if (tv.dtype != "f32" && tv.dtype != "f16")
           throw ContainerError("unknown dtype '" + tv.dtype + "'");
-        for (auto& s : sh->arr) tv.shape.push_back((int64_t)s.num);
+        for (auto& s : sh->arr) {
+          if (s.num < 0) throw ContainerError(path + ": tensor '" + nm->str + "' has a negative dimension");
+          tv.shape.push_back((int64_t)s.num);
+        }
         tv.nbytes = (int64_t)nb->num;
-        int64_t o = (int64_t)off->num;
-        if (tv.nbytes != tv.numel() * (tv.dtype == "f32" ? 4 : 2))
+        const int64_t o = (int64_t)off->num;
+        if (tv.nbytes < 0 || tv.nbytes != tv.numel() * (tv.dtype == "f32" ? 4 : 2))
           throw ContainerError(path + ": tensor '" + nm->str + "' nbytes disagrees with dtype/shape");
-        if (o % 64 != 0) throw ContainerError(path + ": tensor '" + nm->str + "' offset not 64-byte aligned");
-        if (payload + o + tv.nbytes > size_)
+        if (o < 0 || o % 64 != 0)
+          throw ContainerError(path + ": tensor '" + nm->str + "' offset not 64-byte aligned");
+        // overflow-safe bounds (a negative or huge offset cannot wrap around)
+        const uint64_t room = payload <= size_ ? (uint64_t)(size_ - payload) : 0;
+        if ((uint64_t)o > room || (uint64_t)tv.nbytes > room - (uint64_t)o)
           throw ContainerError(path + ": tensor '" + nm->str + "' extends past end of file");
+        if (tensors_.count(nm->str))
+          throw ContainerError(path + ": duplicate tensor names in index");
         tv.data = base_ + payload + o;
         tensors_[nm->str] = tv;
+        regions.push_back({o, o + tv.nbytes});
       }
+    // tensor regions must not overlap (`container.py:316-322`)
+    std::sort(regions.begin(), regions.end());
+    for (size_t i = 1; i < regions.size(); ++i)
+      if (regions[i].first < regions[i - 1].second)
+        throw ContainerError(path + ": tensor regions overlap");
   }
   ~Container() {
     if (base_) munmap((void*)base_, size_);

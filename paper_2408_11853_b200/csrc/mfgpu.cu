@@ -143,6 +143,23 @@ struct Uploader {
 
 }  // namespace
 
+// Kind and tensor-name/shape contract of an opened container (`encoder.py:107-115`).
+static void check_contract(const Container& c) {
+  const Manifest& man = c.manifest();
+  if (man.like != "comet-qe" && man.like != "comet" && man.like != "bleurt")
+    throw Fail{MFG_ERR_CONTAINER, "unknown metric kind '" + man.like + "'"};
+  if (man.d_model <= 0 || man.n_heads <= 0 || man.d_model % man.n_heads != 0)
+    throw Fail{MFG_ERR_CONTAINER, "d_model not divisible by n_heads"};
+  for (auto& kv : required_shapes(man)) {
+    const TensorView* t = c.find(kv.first);
+    if (!t) throw Fail{MFG_ERR_CONTAINER, c.path() + ": missing tensor '" + kv.first + "'"};
+    if (t->shape != kv.second)
+      throw Fail{MFG_ERR_CONTAINER, c.path() + ": tensor '" + kv.first + "' has shape " +
+                                        shape_repr(t->shape) + ", manifest implies " +
+                                        shape_repr(kv.second)};
+  }
+}
+
 struct mfg_ctx {
   int device = 0, precision = MFG_PREC_FP32, num_sms = 148;
   bool split = true, pre_norm = false, profile = false;
@@ -370,22 +387,10 @@ struct mfg_ctx {
     lap("open", 1);
     if (const char* e = getenv("MFG_WEIGHT_PRESCALE")) prescale = e[0] != '0';
     man = c.manifest();
-    if (man.like == "comet-qe") { kind = 0; n_roles = 2; }
-    else if (man.like == "comet") { kind = 1; n_roles = 3; }
-    else if (man.like == "bleurt") { kind = 2; n_roles = 1; }
-    else throw Fail{MFG_ERR_CONTAINER, "unknown metric kind '" + man.like + "'"};
-    if (man.d_model <= 0 || man.n_heads <= 0 || man.d_model % man.n_heads != 0)
-      throw Fail{MFG_ERR_CONTAINER, "d_model not divisible by n_heads"};
+    check_contract(c);
+    kind = man.like == "comet-qe" ? 0 : man.like == "comet" ? 1 : 2;
+    n_roles = kind == 0 ? 2 : kind == 1 ? 3 : 1;
     pre_norm = man.norm_style == "pre";
-    // shape contract (encoder.py:107-115)
-    for (auto& kv : required_shapes(man)) {
-      const TensorView* t = c.find(kv.first);
-      if (!t) throw Fail{MFG_ERR_CONTAINER, c.path() + ": missing tensor '" + kv.first + "'"};
-      if (t->shape != kv.second)
-        throw Fail{MFG_ERR_CONTAINER, c.path() + ": tensor '" + kv.first + "' has shape " +
-                                          shape_repr(t->shape) + ", manifest implies " +
-                                          shape_repr(kv.second)};
-    }
     d = (int)man.d_model;
     dp = padN(d);
     f = (int)man.d_ffn;
@@ -932,6 +937,21 @@ extern "C" int mfg_create(const mfg_config* cfg, mfg_ctx** out) {
     return set_global(MFG_ERR_RUNTIME, e.what());
   }
   *out = c;
+  return set_global(MFG_OK, "");
+}
+
+extern "C" int mfg_check_container(const char* path) {
+  if (!path) return set_global(MFG_ERR_USAGE, "null argument");
+  try {
+    Container c(path);
+    check_contract(c);
+  } catch (const Fail& f) {
+    return set_global(f.code, f.msg);
+  } catch (const ContainerError& e) {
+    return set_global(MFG_ERR_CONTAINER, e.what());
+  } catch (const std::exception& e) {
+    return set_global(MFG_ERR_RUNTIME, e.what());
+  }
   return set_global(MFG_OK, "");
 }
 

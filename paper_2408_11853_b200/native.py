@@ -111,6 +111,8 @@ def gpu():
             lib.mfg_last_error.restype = C.c_int
             lib.mfg_destroy.argtypes = [C.c_void_p]
             lib.mfg_destroy.restype = None
+            lib.mfg_check_container.argtypes = [C.c_char_p]
+            lib.mfg_check_container.restype = C.c_int
             lib.mfg_get_model_info.argtypes = [C.c_void_p, C.POINTER(MfgModelInfo)]
             lib.mfg_get_model_info.restype = C.c_int
             lib.mfg_get_stats.argtypes = [C.c_void_p, C.POINTER(MfgStats)]

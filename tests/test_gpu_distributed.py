@@ -66,3 +66,25 @@ def test_ranks_score_bitwise_like_one_process(fixture_dir, vocab_path, world):
     for r in range(world):
         assert result[r] == solo
     assert np.isfinite(solo).all()
+
+
+def test_bench_self_launches_ranks_through_distributed_evaluator(tmp_path):
+    """`bench.py --gpus 2` outside torchrun re-launches itself with two ranks
+    (MFG_BENCH_BACKEND=gloo lets both share this box's GPU: a code-path check,
+    not a measurement); the e2e leg runs DistributedEvaluator."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+    env = dict(os.environ, MFG_BENCH_BACKEND="gloo", MFG_BENCH_DIR=str(tmp_path))
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "1",
+                        "--steps", "2", "--warmup", "3", "--records-per-step", "512"],
+                       capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["config"]["global_records"] == 1024
+    assert "DistributedEvaluator" in line["e2e"]["path"]
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] > 0

@@ -67,3 +67,43 @@ def test_mfeval_driver_links_and_reports_usage():
     nm = subprocess.run(["nm", "-D", "--undefined-only", str(exe)], capture_output=True, text=True).stdout
     for sym in ("mfh_encode_tsv", "mfh_plan", "mfh_pack_roles", "mfg_create", "mfg_score_batch"):
         assert sym in nm, sym
+
+
+def _container_with_index(tmp_path, patch):
+    """A valid tiny container whose JSON tensor index is rewritten by `patch`."""
+    import json
+    import struct
+
+    from oracle import fixtures as fx
+    from oracle import mfrg
+    man = fx.tiny_manifest("comet-qe")
+    w = fx.fixture_weights(man, 3)
+    path = tmp_path / "c.mfrg"
+    mfrg.write(str(path), mfrg.manifest_dict(**man), [(n, "f32", w[n]) for n, _ in fx.tensor_shapes(man)])
+    raw = path.read_bytes()
+    hlen = struct.unpack("<I", raw[8:12])[0]
+    header = json.loads(raw[12:12 + hlen])
+    payload = raw[(12 + hlen + 63) // 64 * 64:]
+    patch(header["tensors"])
+    hb = json.dumps(header, sort_keys=True, separators=(",", ":")).encode()
+    pad = (-(12 + len(hb))) % 64
+    bad = tmp_path / "bad.mfrg"
+    bad.write_bytes(b"MFRG0001" + struct.pack("<I", len(hb)) + hb + b"\0" * pad + payload)
+    return str(path), str(bad)
+
+
+@pytest.mark.parametrize("what,patch,needle", [
+    ("negative offset", lambda t: t[1].update(offset=-t[1]["nbytes"] // 64 * 64), "offset"),
+    ("past end", lambda t: t[-1].update(offset=t[-1]["offset"] + 1 << 20), "past end"),
+    ("overlap", lambda t: t[1].update(offset=t[0]["offset"]), "overlap"),
+    ("duplicate", lambda t: t[1].update(name=t[0]["name"]), "duplicate"),
+    ("huge offset", lambda t: t[0].update(offset=2 ** 62), "past end"),
+])
+def test_native_container_check_rejects_bad_index(tmp_path, what, patch, needle):
+    """mfg_check_container (host only, the checks mfg_create runs before the GPU)."""
+    lib = native.gpu()
+    good, bad = _container_with_index(tmp_path, patch)
+    assert lib.mfg_check_container(good.encode()) == 0
+    rc = lib.mfg_check_container(bad.encode())
+    code, msg = native.last_error(None)
+    assert rc == 3 and code == 3 and needle in msg, (what, msg)

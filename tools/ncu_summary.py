@@ -1,6 +1,7 @@
 """Summarise an ncu capture + launch list into profiles/ncu_summary_<tag>.json.
 
-    python tools/ncu_summary.py gpurun_out/prof_r01.ncu-rep gpurun_out/launches_r01.csv r01
+    python tools/ncu_summary.py gpurun_out/prof_r01.ncu-rep gpurun_out/launches_r01.csv r01 \
+        [config precision tokens_per_launch]
 
 Per kernel (full-set capture): duration, DRAM read/write bytes, DRAM %, tensor
 pipe %, SM clock, registers, achieved occupancy. From the launch list (one
@@ -78,15 +79,18 @@ def launch_list(path):
             for k, (n, ns) in sorted(agg.items(), key=lambda x: -x[1][1])}, tot / 1e6
 
 
-def main(rep, launches, tag):
+def main(rep, launches, tag, cfg="2", prec="fp32", tokens=None):
     kernels = full_set(rep)
     shares, total_ms = launch_list(launches)
     gemms = [k for k in kernels if k["kernel"].startswith(("gemm_tc_kernel", "gemm2_tc_kernel"))]
     dom = max(gemms, key=lambda k: k.get("duration_ms", 0)) if gemms else None
     summary = {
         "tag": tag,
-        "how": "ncu --set full --clock-control none (first layer of 1 window of 1024 config-2 records, "
-               "tools/profile_window.py); launch list: ncu --metrics gpu__time_duration.sum",
+        "config": int(cfg), "precision": prec,
+        "tokens_per_launch": int(tokens) if tokens else None,
+        "how": f"ncu --set full --clock-control none (first layer of 1 window of config-{cfg} records, "
+               f"precision {prec}, tools/profile_window.py); launch list: ncu --metrics "
+               "gpu__time_duration.sum",
         "window_total_ms_serialised": total_ms,
         "launch_shares": shares,
         "kernels": kernels,
@@ -107,4 +111,4 @@ def main(rep, launches, tag):
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:7])
