@@ -166,12 +166,17 @@ cudaError_t launch_gemm(const CUtensorMap* ah, const CUtensorMap* al, const CUte
                         const CUtensorMap* bl, int bn, int nsplit, int epi, const GemmArgs& a_in,
                         int num_sms, cudaStream_t st) {
   if (a_in.K % GEMM_BK != 0 || a_in.N % bn != 0) return cudaErrorInvalidValue;
-  static const int group_m = [] {
+  // Tile raster. Narrow GEMMs (N <= 1024: O-proj, FFN2) walk groups of 4
+  // M-blocks M-fastest: ncu at config 2 (FFN2, K = 4096, 253k rows) reads 8.2 GB
+  // of DRAM instead of 11.3 GB (algorithmic 5.2 GB) and runs 3.7 % faster alone;
+  // wider GEMMs keep N-fastest (their A tiles are shared by >= 12 concurrent
+  // N-tiles either way). MFG_GEMM_GROUP=G forces G for every GEMM.
+  static const int group_env = [] {
     const char* e = getenv("MFG_GEMM_GROUP");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : -1;
   }();
   GemmArgs a = a_in;
-  a.group_m = group_m;
+  a.group_m = group_env >= 0 ? group_env : (gemm_uses_pair(bn) && a.N / bn <= 4 ? 4 : 0);
   const bool split = nsplit == 2;
   if (!gemm_uses_pair(bn) || a.partial == nullptr) a.kchunk = 0;
   if (gemm_uses_pair(bn))

@@ -108,3 +108,20 @@ def test_multi_rank_cli_streams_stdin_like_one_gpu(tiny_factory, tmp_path):
     r = _multi(*base, "--stdin", "--gpus", "2", stdin=bad)
     assert r.returncode == 2 and "line 650: expected 3 tab-separated columns, got 2" in r.stderr
     assert r.stdout == "" and r.stderr.count("error:") == 1
+
+
+@pytest.mark.gpu
+def test_stdin_stream_bad_line_index_matches_list_path(tiny_factory):
+    """A bad line deep in a long stdin stream (many windows in) reports the same
+    global index as the list path (`evaluate.py:117-123`), and nothing reaches stdout."""
+    import paper_2408_11853_b200 as mf
+    fix = tiny_factory("comet-qe", "post", 1234)
+    lines = fx.fixture_tsv_lines("comet-qe", 30000, seed=5)
+    lines[29876] = "one column only"
+    with mf.Evaluator(mf.EvaluatorConfig(model=fix.model, vocab=fix.vocab, quiet=True)) as ev:
+        with pytest.raises(mf.errors.ColumnCountError) as ei:
+            ev.evaluate_lines(lines)
+    assert ei.value.line_index == 29876
+    r = cli("-m", fix.model, "-v", fix.vocab, "--stdin", stdin="".join(l + "\n" for l in lines))
+    assert r.returncode == 2 and r.stdout == ""
+    assert "line 29876: expected 2 tab-separated columns, got 1" in r.stderr
