@@ -36,13 +36,15 @@ def run(cfg, n, extra):
         p = subprocess.Popen([sys.executable, "-m", "paper_2408_11853_b200.cli", "-m", model,
                               "-v", vocab, "--stdin", "--quiet", "-o", out, *extra],
                              stdin=fin, cwd=ROOT)
-        hwm = 0
+        hwm = last = 0
         while p.poll() is None:
             try:
                 with open(f"/proc/{p.pid}/status") as st:
                     for line in st:
                         if line.startswith("VmHWM:"):
                             hwm = max(hwm, int(line.split()[1]))
+                        elif line.startswith("VmRSS:"):
+                            last = int(line.split()[1])  # steady state while scoring
             except OSError:
                 pass
             time.sleep(0.2)
@@ -51,7 +53,8 @@ def run(cfg, n, extra):
     n_out = sum(1 for _ in open(out))
     return {"config": cfg, "lines": n, "rc": p.returncode, "scores": n_out,
             "input_mb": os.path.getsize(path) / 2 ** 20, "peak_rss_mb": hwm / 1024,
-            "wall_s": dt, "records_per_s": n / dt, "scores_sha256_16": digest}
+            "wall_s": dt, "records_per_s": n / dt, "final_rss_mb": last / 1024,
+            "scores_sha256_16": digest}
 
 
 if __name__ == "__main__":
