@@ -34,7 +34,7 @@ struct AlCfg {
   static constexpr int OP = NPL * (AL_TILE + (TAIL ? AL_TTILE : 0));  // one operand (Q, K or V)
   static constexpr int Q_OFF = 0, K_OFF = OP, V_OFF = 2 * OP;
   static constexpr int BAR_OFF = 3 * OP;
-  static constexpr int SMEM = 1024 + BAR_OFF + 128;
+  static constexpr int SMEM = 1024 + BAR_OFF + 128;  // 6 barriers + TMEM slot
 };
 
 __device__ __forceinline__ void al_tmem_st_8(uint32_t taddr, const uint32_t (&r)[8]) {
@@ -86,12 +86,13 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
-  uint64_t* b_load = bars;      // TMA bytes
+  uint64_t* b_lk = bars;        // TMA bytes: Q (first phase) and K blocks
   uint64_t* b_s = bars + 1;     // S MMAs done
   uint64_t* b_sm = bars + 2;    // softmax warps done with S (stats or P written), 128 arrivals
   uint64_t* b_o = bars + 3;     // P·V MMAs of a block done
   uint64_t* b_fin = bars + 4;   // last P·V done
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 5);
+  uint64_t* b_lv = bars + 5;    // TMA bytes: V blocks
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int2 w = work[blockIdx.x / heads];
@@ -102,11 +103,12 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
   const int cq = h * DH, ck = d + h * DH, cv = 2 * d + h * DH;
 
   if (tid == 0) {
-    mbar_init(b_load, 1);
+    mbar_init(b_lk, 1);
     mbar_init(b_s, 1);
     mbar_init(b_sm, 128);
     mbar_init(b_o, 1);
     mbar_init(b_fin, 1);
+    mbar_init(b_lv, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<256>(tslot);
@@ -117,27 +119,35 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      uint32_t ph_load = 0, ph_sm = 0, ph_o = 0;
-      auto load_wait = [&](uint32_t bytes) {
-        mbar_wait(b_load, ph_load);
-        ph_load ^= 1;
-        (void)bytes;
-      };
+      // Each K block is loaded as soon as the previous S has read the K buffer,
+      // each V block as soon as the previous P·V has read the V buffer, so the
+      // loads run under the softmax instead of in front of every block.
+      uint32_t ph_k = 0, ph_v = 0, ph_s = 0, ph_sm = 0, ph_o = 0;
       const uint32_t op_bytes = 128 * (128 + (TAIL ? 32 : 0)) * C::NPL;
-      mbar_expect_tx(b_load, op_bytes);
-      al_load<SPLIT, TAIL>(sm + C::Q_OFF, &mh, &ml, &th, &tl, b_load, cq, start + q0);
-      load_wait(op_bytes);
+      auto load_k = [&](int kb) {
+        mbar_expect_tx(b_lk, op_bytes);
+        al_load<SPLIT, TAIL>(sm + C::K_OFF, &mh, &ml, &th, &tl, b_lk, ck, start + kb * 128);
+      };
+      auto load_v = [&](int kb) {
+        mbar_expect_tx(b_lv, op_bytes);
+        al_load<SPLIT, TAIL>(sm + C::V_OFF, &mh, &ml, &th, &tl, b_lv, cv, start + kb * 128);
+      };
+      // Q rides on K(0)'s phase (one arrive.expect_tx per phase: the barrier counts 1)
+      mbar_expect_tx(b_lk, 2 * op_bytes);
+      al_load<SPLIT, TAIL>(sm + C::Q_OFF, &mh, &ml, &th, &tl, b_lk, cq, start + q0);
+      al_load<SPLIT, TAIL>(sm + C::K_OFF, &mh, &ml, &th, &tl, b_lk, ck, start);
       const uint8_t* qt = sm + C::Q_OFF;
       const uint8_t* kt = sm + C::K_OFF;
       const uint8_t* vt = sm + C::V_OFF;
       for (int pass = 0; pass < 2; ++pass) {
         for (int kb = 0; kb < nkb; ++kb) {
           const int nk = min(128, L - kb * 128), n16 = (nk + 15) & ~15;
-          mbar_expect_tx(b_load, op_bytes * (pass ? 2 : 1));
-          al_load<SPLIT, TAIL>(sm + C::K_OFF, &mh, &ml, &th, &tl, b_load, ck, start + kb * 128);
-          if (pass)
-            al_load<SPLIT, TAIL>(sm + C::V_OFF, &mh, &ml, &th, &tl, b_load, cv, start + kb * 128);
-          load_wait(0);
+          mbar_wait(b_lk, ph_k);  // K(kb) landed
+          ph_k ^= 1;
+          if (pass) {
+            mbar_wait(b_lv, ph_v);  // V(kb) landed
+            ph_v ^= 1;
+          }
           tc_fence_after();
           // ---- S = Q·K_blockᵀ
           const uint32_t idesc = idesc_f16kind(128, n16, fmt);
@@ -163,6 +173,13 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
             }
           }
           tc_commit(b_s);
+          mbar_wait(b_s, ph_s);  // S done: the K buffer is free
+          ph_s ^= 1;
+          if (kb + 1 < nkb) load_k(kb + 1);
+          else if (pass == 0) {
+            load_k(0);  // pass 2 starts over; the V buffer has not been used yet
+            load_v(0);
+          }
           mbar_wait(b_sm, ph_sm);  // softmax read S (pass 1) / wrote P (pass 2)
           ph_sm ^= 1;
           tc_fence_after();
@@ -189,6 +206,7 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
             if (kb + 1 < nkb) {  // P (S columns) and V are overwritten by the next block
               mbar_wait(b_o, ph_o);
               ph_o ^= 1;
+              load_v(kb + 1);
             }
           }
         }
