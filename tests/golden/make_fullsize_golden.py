@@ -55,7 +55,8 @@ def score(path, vocab, lines, mode):
 
 def main(cfgs):
     os.makedirs(WORK, exist_ok=True)
-    for mode in ("fp32", "fp16"):
+    modes = os.environ.get("MFG_GOLDEN_MODES", "fp32,fp16").split(",")
+    for mode in modes:
         for cfg in cfgs:
             dst = os.path.join(HERE, f"fullsize_cfg{cfg}.json")
             out = json.load(open(dst)) if os.path.exists(dst) else {}
