@@ -31,9 +31,13 @@ struct AlCfg {
   static constexpr bool SPLIT = MODE == 3;
   static constexpr bool TAIL = DH == 80;
   static constexpr int NPL = SPLIT ? 2 : 1;
-  static constexpr int OP = NPL * (AL_TILE + (TAIL ? AL_TTILE : 0));  // one operand (Q, K or V)
+  static constexpr int OP = NPL * (AL_TILE + (TAIL ? AL_TTILE : 0));  // Q or K
+  // V for DH 80: per plane two 64-column 128B-swizzled atoms (dims 0..63, 64..127)
+  // so P·V is one N=80 MN-major product per operand pair
+  static constexpr int VPL = TAIL ? 2 * AL_TILE : AL_TILE;
+  static constexpr int VOP = NPL * VPL;
   static constexpr int Q_OFF = 0, K_OFF = OP, V_OFF = 2 * OP;
-  static constexpr int BAR_OFF = 3 * OP;
+  static constexpr int BAR_OFF = 2 * OP + VOP;
   static constexpr int SMEM = 1024 + BAR_OFF + 128;  // 6 barriers + TMEM slot
 };
 
@@ -51,6 +55,22 @@ __device__ __forceinline__ void al_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+
+// 128 rows of V (column block `col`) starting at token `tok0`, DH 80 as two
+// 64-column atoms per plane (the second past the tensor's last column is zero-filled).
+template <bool SPLIT, bool TAIL>
+__device__ __forceinline__ void al_load_v(uint8_t* dst, const CUtensorMap* mh, const CUtensorMap* ml,
+                                          uint64_t* bar, int col, int tok0) {
+  constexpr int VPL = TAIL ? 2 * AL_TILE : AL_TILE;
+  for (int r0 = 0; r0 < 128; r0 += 32) {
+    tma_load_2d(dst + r0 * 128, mh, bar, col, tok0 + r0);
+    if (SPLIT) tma_load_2d(dst + VPL + r0 * 128, ml, bar, col, tok0 + r0);
+    if (TAIL) {
+      tma_load_2d(dst + AL_TILE + r0 * 128, mh, bar, col + 64, tok0 + r0);
+      if (SPLIT) tma_load_2d(dst + VPL + AL_TILE + r0 * 128, ml, bar, col + 64, tok0 + r0);
+    }
+  }
 }
 
 // 128 rows of one operand (Q, K or V column block `col`) starting at token `tok0`:
@@ -129,8 +149,8 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
         al_load<SPLIT, TAIL>(sm + C::K_OFF, &mh, &ml, &th, &tl, b_lk, ck, start + kb * 128);
       };
       auto load_v = [&](int kb) {
-        mbar_expect_tx(b_lv, op_bytes);
-        al_load<SPLIT, TAIL>(sm + C::V_OFF, &mh, &ml, &th, &tl, b_lv, cv, start + kb * 128);
+        mbar_expect_tx(b_lv, 128 * (TAIL ? 256 : 128) * C::NPL);
+        al_load_v<SPLIT, TAIL>(sm + C::V_OFF, &mh, &ml, b_lv, cv, start + kb * 128);
       };
       // Q rides on K(0)'s phase (one arrive.expect_tx per phase: the barrier counts 1)
       mbar_expect_tx(b_lk, 2 * op_bytes);
@@ -185,22 +205,21 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
           tc_fence_after();
           if (pass) {
             // ---- O += P·V_block (A = P from TMEM, B = V MN-major)
-            const uint32_t idesc64 = idesc_f16kind(128, 64, fmt) | (1u << 16);
-            const uint32_t idesc16 = idesc_f16kind(128, 16, fmt) | (1u << 16);
-            const uint8_t* vtt = vt + C::NPL * AL_TILE;
+            // DH 80: one N=80 product (B spans the plane's two atoms, LBO = atom
+            // stride) writing O columns 128..207 (dims 0..79)
+            const uint32_t idescv = idesc_f16kind(128, DH, fmt) | (1u << 16);
             for (int kk = 0; kk < n16; kk += 16) {
               const uint32_t pa = tm + 32 * (kk >> 5) + 8 * ((kk >> 4) & 1);
               const uint32_t acc0 = (kb | kk) != 0;
-              const uint64_t vh = umma_desc_sw128(vt + kk * 128);
-              al_mma_ts(tm + 128, pa, vh, idesc64, acc0);
-              if (PSPLIT) al_mma_ts(tm + 128, pa + 16, vh, idesc64, 1);
-              if (SPLIT) al_mma_ts(tm + 128, pa, umma_desc_sw128(vt + AL_TILE + kk * 128), idesc64, 1);
-              if (TAIL) {
-                const uint64_t vht = umma_desc_sw32(vtt + kk * 32);
-                al_mma_ts(tm + 192, pa, vht, idesc16, acc0);
-                if (PSPLIT) al_mma_ts(tm + 192, pa + 16, vht, idesc16, 1);
-                if (SPLIT) al_mma_ts(tm + 192, pa, umma_desc_sw32(vtt + AL_TTILE + kk * 32), idesc16, 1);
-              }
+              const uint64_t vh = TAIL ? umma_desc_sw128_mn(vt + kk * 128, AL_TILE)
+                                       : umma_desc_sw128(vt + kk * 128);
+              al_mma_ts(tm + 128, pa, vh, idescv, acc0);
+              if (PSPLIT) al_mma_ts(tm + 128, pa + 16, vh, idescv, 1);
+              if (SPLIT)
+                al_mma_ts(tm + 128, pa,
+                          TAIL ? umma_desc_sw128_mn(vt + C::VPL + kk * 128, AL_TILE)
+                               : umma_desc_sw128(vt + AL_TILE + kk * 128),
+                          idescv, 1);
             }
             tc_commit(kb + 1 == nkb ? b_fin : b_o);
             if (kb + 1 < nkb) {  // P (S columns) and V are overwritten by the next block

@@ -69,7 +69,10 @@ struct AtqCfg {
   static constexpr int NPL_QK = SPLIT ? 4 : 2;  // Qh Kh (Ql Kl)
   static constexpr int NPL_V = SPLIT ? 2 : 1;   // Vh (Vl)
   static constexpr int QK_BYTES = NPL_QK * (ATQ_TILE + (TAIL ? ATQ_TTILE : 0));
-  static constexpr int V_BYTES = NPL_V * (ATQ_TILE + (TAIL ? ATQ_TTILE : 0));
+  // V for DH 80: per plane two 128B-swizzled 64-column atoms (dims 0..63 and
+  // 64..127 of the head's column block; only 64..79 are used), so P·V is ONE
+  // N=80 MN-major product per plane instead of an N=64 + an N=16 one
+  static constexpr int V_BYTES = NPL_V * (TAIL ? 2 * ATQ_TILE : ATQ_TILE);
   static constexpr int QK_ST = SPLIT ? 2 : 3;
   static constexpr int V_ST = SPLIT ? (TAIL ? 1 : 3) : (TAIL ? 3 : 5);
   static constexpr int BAR_OFF = QK_ST * QK_BYTES + V_ST * V_BYTES;
@@ -307,18 +310,18 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
         {
           const int s = k % C::V_ST;
           mbar_wait(&v_empty[s], ((k / C::V_ST) & 1) ^ 1);
-          mbar_expect_tx(&v_full[s], rows32 * row_bytes * C::NPL_V);
+          mbar_expect_tx(&v_full[s], rows32 * (TAIL ? 256 : 128) * C::NPL_V);
           uint8_t* t = sm + C::QK_ST * C::QK_BYTES + s * C::V_BYTES;
-          uint8_t* tt = t + C::NPL_V * ATQ_TILE;
+          constexpr int VPL = TAIL ? 2 * ATQ_TILE : ATQ_TILE;  // bytes per V plane
           int o = 0;
           for (int j = 0; j < 4; ++j) {
             for (int r0 = 0; r0 < tl.len[j]; r0 += 32, o += 32) {
               const int tok = tl.t0[j] + r0;
               tma_load_2d(t + o * 128, &mh, &v_full[s], cv, tok);
-              if (SPLIT) tma_load_2d(t + ATQ_TILE + o * 128, &ml, &v_full[s], cv, tok);
-              if (TAIL) {
-                tma_load_2d(tt + o * 32, &th, &v_full[s], cv + 64, tok);
-                if (SPLIT) tma_load_2d(tt + ATQ_TTILE + o * 32, &tl_, &v_full[s], cv + 64, tok);
+              if (SPLIT) tma_load_2d(t + VPL + o * 128, &ml, &v_full[s], cv, tok);
+              if (TAIL) {  // dims 64..127 (past the tensor's last column: zero-filled)
+                tma_load_2d(t + ATQ_TILE + o * 128, &mh, &v_full[s], cv + 64, tok);
+                if (SPLIT) tma_load_2d(t + VPL + ATQ_TILE + o * 128, &ml, &v_full[s], cv + 64, tok);
               }
             }
           }
@@ -384,25 +387,18 @@ __global__ void __launch_bounds__(ATQ_THREADS, 1)
         const uint32_t idesc128 = idesc_f16kind(128, 128, fmt) | (1u << 16);
         uint8_t* t = sm + C::QK_ST * C::QK_BYTES + s * C::V_BYTES;
         const uint32_t tp = tm + b * 128, to = tm + ocol(k);
-        const uint32_t idesc16 = idesc_f16kind(128, 16, fmt) | (1u << 16);
-        uint8_t* tt = t + C::NPL_V * ATQ_TILE;
+        const uint32_t idesc80 = idesc_f16kind(128, 80, fmt) | (1u << 16);
         for (int kk = 0; kk < n16; kk += 16) {
           const uint32_t ph_ = tp + 32 * (kk >> 5) + 8 * ((kk >> 4) & 1);
           const uint64_t vh = umma_desc_sw128(t + kk * 128);
           if (TAIL) {
-            // DH 80: O[0,64) from the main V tiles, O[64,80) from the tail tiles;
-            // hi·hi + lo·hi + hi·lo each (the [Vh | Vl] merge would need 160 columns)
-            const uint64_t vht = umma_desc_sw32_mn(tt + kk * 32);
-            tc_mma_ts(to, ph_, vh, idesc64, kk != 0);
-            tc_mma_ts(to + 64, ph_, vht, idesc16, kk != 0);
-            if (PSPLIT) {
-              tc_mma_ts(to, ph_ + 16, vh, idesc64, 1);
-              tc_mma_ts(to + 64, ph_ + 16, vht, idesc16, 1);
-            }
-            if (SPLIT) {
-              tc_mma_ts(to, ph_, umma_desc_sw128(t + ATQ_TILE + kk * 128), idesc64, 1);
-              tc_mma_ts(to + 64, ph_, umma_desc_sw32_mn(tt + ATQ_TTILE + kk * 32), idesc16, 1);
-            }
+            // DH 80: O[0,80) = P·V as one N=80 product per operand pair, B spanning
+            // the plane's two 64-column atoms (LBO = atom stride); hi·hi + lo·hi + hi·lo
+            const uint64_t v80h = umma_desc_sw128_mn(t + kk * 128, ATQ_TILE);
+            tc_mma_ts(to, ph_, v80h, idesc80, kk != 0);
+            if (PSPLIT) tc_mma_ts(to, ph_ + 16, v80h, idesc80, 1);
+            if (SPLIT)
+              tc_mma_ts(to, ph_, umma_desc_sw128_mn(t + 2 * ATQ_TILE + kk * 128, ATQ_TILE), idesc80, 1);
           } else {
             if (SPLIT)
               tc_mma_ts(to, ph_, umma_desc_sw128_mn(t + kk * 128, ATQ_TILE), idesc128, kk != 0);

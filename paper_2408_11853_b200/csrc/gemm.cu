@@ -166,17 +166,26 @@ cudaError_t launch_gemm(const CUtensorMap* ah, const CUtensorMap* al, const CUte
                         const CUtensorMap* bl, int bn, int nsplit, int epi, const GemmArgs& a_in,
                         int num_sms, cudaStream_t st) {
   if (a_in.K % GEMM_BK != 0 || a_in.N % bn != 0) return cudaErrorInvalidValue;
-  // Tile raster. Narrow GEMMs (N <= 1024: O-proj, FFN2) walk groups of 4
-  // M-blocks M-fastest: ncu at config 2 (FFN2, K = 4096, 253k rows) reads 8.2 GB
-  // of DRAM instead of 11.3 GB (algorithmic 5.2 GB) and runs 3.7 % faster alone;
-  // wider GEMMs keep N-fastest (their A tiles are shared by >= 12 concurrent
-  // N-tiles either way). MFG_GEMM_GROUP=G forces G for every GEMM.
+  // Tile raster (profiles/gemm_raster_r03.txt, measured per GEMM with ncu):
+  //  * narrow (N <= 1024: config-2 O-proj, FFN2): groups of 4 M-blocks M-fastest —
+  //    FFN2 DRAM 11.3 -> 8.2 GB per launch (algorithmic 5.2 GB), 3.7 % faster alone;
+  //  * wide GEMMs whose weight does not stay L2-resident (> 48 MB of pieces, >= 16
+  //    N-tiles: XLM-R XL QKV 79 MB, FFN1 105 MB): groups of 16 M-blocks, so a few
+  //    N-tiles' weights are shared by 16 concurrent M-blocks instead of every
+  //    M-block sweeping the whole weight — FFN1 DRAM read 88 -> 65 GB, -5.6 %;
+  //  * otherwise N-fastest (an M-block's A is shared by its concurrent N-tiles).
+  // MFG_GEMM_GROUP=G forces G for every GEMM.
   static const int group_env = [] {
     const char* e = getenv("MFG_GEMM_GROUP");
     return e ? atoi(e) : -1;
   }();
   GemmArgs a = a_in;
-  a.group_m = group_env >= 0 ? group_env : (gemm_uses_pair(bn) && a.N / bn <= 4 ? 4 : 0);
+  const int num_n = a.N / bn;
+  const double w_bytes = (double)a.N * a.K * (nsplit == 2 ? 4 : 2);
+  int group = 0;
+  if (gemm_uses_pair(bn) && num_n <= 4) group = 4;
+  else if (gemm_uses_pair(bn) && num_n >= 16 && w_bytes > 48e6) group = 16;
+  a.group_m = group_env >= 0 ? group_env : group;
   const bool split = nsplit == 2;
   if (!gemm_uses_pair(bn) || a.partial == nullptr) a.kchunk = 0;
   if (gemm_uses_pair(bn))

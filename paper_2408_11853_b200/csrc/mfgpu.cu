@@ -189,6 +189,22 @@ struct mfg_ctx {
   int cap_records = 0;
   float *x32 = nullptr, *y32 = nullptr;
   float* gemm_part = nullptr;  // K-chunk running sums of the CTA-pair GEMM (GemmArgs::partial)
+  bool part_persist = false;   // gemm_part pinned in L2 (persisting window on the launch stream)
+
+  void apply_l2_window(cudaStream_t s) {
+    if (!part_persist || !s) return;
+    int max_win = 0;
+    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, device);
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.base_ptr = gemm_part;
+    v.accessPolicyWindow.num_bytes =
+        std::min(gemm_partial_floats(num_sms) * sizeof(float), (size_t)std::max(0, max_win));
+    v.accessPolicyWindow.hitRatio = 1.0f;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    if (cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess)
+      cudaGetLastError();  // best effort: only the DRAM traffic changes, never the results
+  }
   Act xa, ca, ha, fa, qa;          // qa: Q|K|V pieces [T][qkv_ld]
   // last layer on BOS rows only (one row per sequence): ctx, residual/LN, FFN hidden, Q
   Act cb, xb, hb, qb;
@@ -492,6 +508,26 @@ struct mfg_ctx {
     cap_records = cfg.max_records > 0 ? cfg.max_records : 4096;
     x32 = dalloc<float>((size_t)cap_tokens * dp);
     gemm_part = dalloc<float>(gemm_partial_floats(num_sms));
+    // K-chunked GEMMs (K > 4096, or XL's 2560) round-trip their fp32 chunk sums
+    // through gemm_part once per chunk and tile; under the activation and weight
+    // streams those lines were evicted to DRAM between the drain and the next
+    // read (ncu, config 5: ~60 GB of extra DRAM traffic per layer). Pin the
+    // buffer in L2 as a persisting access-policy window on the launch stream.
+    part_persist = (gemm_kchunk_blocks(dp) > 0 || gemm_kchunk_blocks(fp) > 0) &&
+                   !(getenv("MFG_L2_PERSIST") && getenv("MFG_L2_PERSIST")[0] == '0');
+    if (part_persist) {
+      int max_persist = 0;
+      cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+      const size_t want = gemm_partial_floats(num_sms) * sizeof(float);
+      if (max_persist <= 0 ||
+          cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(want, (size_t)max_persist)) !=
+              cudaSuccess) {
+        part_persist = false;
+        cudaGetLastError();
+      } else {
+        apply_l2_window(st);
+      }
+    }
     y32 = dalloc<float>((size_t)cap_tokens * dp);
     make_act(qa, cap_tokens, qkv_ld, split);
     {
@@ -898,6 +934,7 @@ struct mfg_ctx {
 
   ~mfg_ctx() {
     if (st) cudaStreamSynchronize(st);
+    if (part_persist) cudaCtxResetPersistingL2Cache();  // release the pinned lines
     delete twin;
     for (void* p : allocs) cudaFree(p);
     if (h_ids) cudaFreeHost(h_ids);
@@ -1000,6 +1037,7 @@ extern "C" int mfg_set_stream(mfg_ctx* c, void* stream) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
   c->st = stream ? (cudaStream_t)stream : c->own_st;
+  c->apply_l2_window(c->st);
   return MFG_OK;
 }
 
