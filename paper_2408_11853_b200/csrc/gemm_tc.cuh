@@ -59,6 +59,8 @@ struct GemmArgs {
                              // product to fp16, add the fp16 bias in fp16, round residual
                              // sums to fp16 (bias must hold fp16-representable values)
   int kchunk;                // CTA-pair kernel: k-blocks per fresh TMEM accumulator (0 = all K).
+  int* tile_ctr;             // CTA-pair kernel: zeroed tile counter -> tiles handed out in index
+                             // order as pairs free up (null: static round-robin)
   float* partial;            // [gridDim.x][256/4][128][4] fp32: running sum of the finished chunks
                              // (the tcgen05 accumulator rounds each MMA's add toward zero, so
                              // error grows with the adds per accumulator; chunk sums are
@@ -94,7 +96,8 @@ constexpr int GEMM_SMEM_LIMIT = 232448;  // 227 KB opt-in dynamic smem
 // row (8 lanes writing or reading float4 hit 8 distinct bank quads)
 constexpr int GEMM_EPI_STRIDE = 32;
 constexpr int GEMM_EPI_BYTES = GEMM_EPI_WARPS * 32 * GEMM_EPI_STRIDE * 4;
-constexpr int GEMM_BAR_BYTES = 256;
+constexpr int GEMM_BAR_BYTES = 320;
+constexpr int TRING = 4;  // CTA-pair kernel: tile-id ring depth
 
 template <int BN, bool SPLIT>
 struct GemmCfg {
@@ -515,12 +518,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tr_full = tempty + 2;           // [TRING] tile id published (both CTAs)
+  uint64_t* tr_empty = tr_full + TRING;     // [TRING] every consumer read it (leader only)
+  int* tring = reinterpret_cast<int*>(tr_empty + TRING);  // [TRING] tile ids, -1 = done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tring + TRING);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  // Tile hand-out. The leader's producer thread takes the next tile (an atomic
+  // counter: tiles start in index order as pairs free up, so the pairs that share
+  // an A block or a weight slice stream it at the same time and hit in L2; the
+  // static round-robin drifted apart over long K loops) and publishes it to a
+  // TRING-deep ring in both CTAs; every other role reads the ids from its ring.
+  auto ring_get = [&](int i, bool leader_release) -> int {
+    const int slot = i % TRING;
+    mbar_wait_cluster(&tr_full[slot], (uint32_t)(i / TRING) & 1);
+    const int t = *(volatile int*)&tring[slot];
+    if (leader_release) mbar_arrive(&tr_empty[slot]);
+    else mbar_arrive_cluster(mapa_shared(&tr_empty[slot], 0));
+    return t;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mapAh);
@@ -536,6 +555,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * C::EPI_WARPS);
+    }
+    for (int r = 0; r < TRING; ++r) {
+      mbar_init(&tr_full[r], 1);
+      // leader's MMA warp + rank 1's producer + both CTAs' epilogue warps
+      mbar_init(&tr_empty[r], 2 + 2 * C::EPI_WARPS);
     }
     fence_mbar_init();
   }
@@ -561,7 +585,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = pair; tile < tiles; tile += npairs) {
+      const uint32_t tring_peer = mapa_shared(tring, 1), trfull_peer = mapa_shared(tr_full, 1);
+      for (int i = 0;; ++i) {
+        int tile;
+        if (rank == 0) {  // take the next tile and publish it to both CTAs' rings
+          tile = args.tile_ctr ? atomicAdd(args.tile_ctr, 1) : pair + i * npairs;
+          if (tile >= tiles) tile = -1;
+          const int slot = i % TRING;
+          mbar_wait_cluster(&tr_empty[slot], ((uint32_t)(i / TRING) & 1) ^ 1);
+          tring[slot] = tile;
+          st_shared_cluster_s32(tring_peer + 4 * slot, tile);
+          mbar_arrive(&tr_full[slot]);
+          mbar_arrive_cluster(trfull_peer + 8 * slot);
+        } else {
+          tile = ring_get(i, false);
+        }
+        if (tile < 0) {
+          // the last pair to finish re-arms the counter for the next launch (every
+          // leader's final atomicAdd on tile_ctr[0] precedes its count here)
+          if (rank == 0 && args.tile_ctr && atomicAdd(args.tile_ctr + 1, 1) == npairs - 1) {
+            atomicExch(args.tile_ctr, 0);
+            atomicExch(args.tile_ctr + 1, 0);
+          }
+          break;
+        }
         int mt, nt;
         tile_mn(tile, num_m, num_n, args.group_m, mt, nt);
         const int m0 = mt * 2 * GEMM_BM + rank * GEMM_BM;
@@ -599,7 +646,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
       int acc = 0;
       uint32_t acc_phase = 0;
       const int kc = args.kchunk > 0 ? args.kchunk : kblocks;
-      for (int tile = pair; tile < tiles; tile += npairs) {
+      for (int i = 0;; ++i) {
+        if (ring_get(i, true) < 0) break;
         for (int cb = 0; cb < kblocks; cb += kc) {  // one fresh accumulator per K chunk
           const int ce = min(kblocks, cb + kc);
           mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -646,7 +694,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
     epi_dispatch(args, [&](auto fmt_c, auto r16_c) {
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = pair; tile < tiles; tile += npairs) {
+      for (int i = 0;; ++i) {
+        int tile = 0;
+        if (lane == 0) tile = ring_get(i, rank == 0);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        if (tile < 0) break;
         int mt, nt;
         tile_mn(tile, num_m, num_n, args.group_m, mt, nt);
         const int m0 = mt * 2 * GEMM_BM + rank * GEMM_BM;

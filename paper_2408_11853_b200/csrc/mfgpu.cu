@@ -190,6 +190,8 @@ struct mfg_ctx {
   float *x32 = nullptr, *y32 = nullptr;
   float* gemm_part = nullptr;  // K-chunk running sums of the CTA-pair GEMM (GemmArgs::partial)
   bool part_persist = false;   // gemm_part pinned in L2 (persisting window on the launch stream)
+  int* tile_ctr = nullptr;     // CTA-pair GEMM tile counter + finished-pair count (self-resetting)
+  bool dyn_tiles = !(getenv("MFG_TILE_DYN") && getenv("MFG_TILE_DYN")[0] == '0');  // A/B switch
 
   void apply_l2_window(cudaStream_t s) {
     if (!part_persist || !s) return;
@@ -508,6 +510,7 @@ struct mfg_ctx {
     cap_records = cfg.max_records > 0 ? cfg.max_records : 4096;
     x32 = dalloc<float>((size_t)cap_tokens * dp);
     gemm_part = dalloc<float>(gemm_partial_floats(num_sms));
+    tile_ctr = dalloc<int>(2);
     // K-chunked GEMMs (K > 4096, or XL's 2560) round-trip their fp32 chunk sums
     // through gemm_part once per chunk and tile; under the activation and weight
     // streams those lines were evicted to DRAM between the drain and the next
@@ -592,6 +595,7 @@ struct mfg_ctx {
     g.alpha = w.alpha;
     g.kchunk = gemm_kchunk_blocks(w.Kpad);
     g.partial = gemm_part;
+    g.tile_ctr = dyn_tiles ? tile_ctr : nullptr;
     g.residual = res;
     g.ldr = ldr;
     if (res16) {
@@ -1216,6 +1220,7 @@ extern "C" int mfgt_gemm(int32_t precision, int32_t epi, int32_t M, int32_t N, i
     g.r16 = r16;
     g.kchunk = gemm_kchunk_blocks(Kp);
     g.partial = s.alloc<float>(gemm_partial_floats(sms));
+    g.tile_ctr = s.alloc<int>(2);
     CK(launch_gemm(&mah, split ? &mal : &mah, &mwh, split ? &mwl : &mwh, bn, split ? 2 : 1, epi,
                    g, sms, 0));
     CK(cudaDeviceSynchronize());

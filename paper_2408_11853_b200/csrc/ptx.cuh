@@ -91,6 +91,27 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// Store a 32-bit value into another CTA's shared memory (shared::cluster address).
+__device__ __forceinline__ void st_shared_cluster_s32(uint32_t cluster_addr, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+// Wait with cluster-scope acquire: data written by another CTA before its
+// release.cluster arrive on this (local) barrier is visible afterwards.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+        : "memory");
+    if (ok) return;
+    if (clock64() - t0 > (1ll << 33)) __trap();
+  }
+}
 // Relaxed remote arrive: no release of this thread's earlier global stores (no
 // membar wait for their completion). For "TMEM accumulator drained" signals,
 // whose only hazard is the TMEM reads, already complete after tcgen05.wait::ld.
