@@ -14,6 +14,9 @@ timeout 900 ncu --profile-from-start off --set full --clock-control none --impor
   -k regex:"gemm2|attention_tc|layernorm" -c 6 -f -o gpurun_out/prof_$TAG python tools/profile_window.py >> gpurun_out/pw_$TAG.log 2>&1
 TOK=$(grep -o "[0-9]* tokens" gpurun_out/pw_$TAG.log | head -1 | cut -d' ' -f1)
 python tools/ncu_summary.py gpurun_out/prof_$TAG.ncu-rep gpurun_out/launches_$TAG.csv $TAG $MFG_CFG $MFG_PREC $TOK
+cp profiles/ncu_summary_$TAG.json gpurun_out/
+# gpurun copies back at most 64 MiB: keep the full capture only when asked
+[ -z "$KEEP_REP" ] && rm -f gpurun_out/prof_$TAG.ncu-rep
 if [ -n "$RASTER" ]; then
   for G in 0 2 4 8 16; do
     MFG_GEMM_GROUP=$G timeout 300 ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
