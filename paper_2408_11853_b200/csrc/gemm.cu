@@ -122,7 +122,13 @@ template <bool SPLIT, int EPI>
 static cudaError_t run2(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* bh,
                         const CUtensorMap* bl, const GemmArgs& a, int num_sms, cudaStream_t st) {
   using C = Gemm2Cfg<SPLIT>;
-  auto kern = gemm2_tc_kernel<SPLIT, EPI>;
+  // single-MMA kernels (16 epilogue warps, 96 registers) get their epilogue
+  // variant fixed at compile time: the binary16 mode then needs no lo-plane
+  // residual registers and does not spill in the epilogue loop
+  auto kern = SPLIT ? gemm2_tc_kernel<SPLIT, EPI, 0>
+              : a.fmt == FMT_F16 && a.r16 ? gemm2_tc_kernel<SPLIT, EPI, 1>
+              : a.fmt == FMT_BF16 ? gemm2_tc_kernel<SPLIT, EPI, 2>
+                                  : gemm2_tc_kernel<SPLIT, EPI, 0>;
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
   if (e != cudaSuccess) return e;

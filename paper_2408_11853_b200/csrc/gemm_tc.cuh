@@ -146,13 +146,19 @@ __device__ __forceinline__ void epi_tile_t(const GemmArgs& args, uint32_t tacc, 
     const int col = n0 + c + 4 * cg;
     // prefetch this chunk's residual (8 x float4, or 8 x (hi, lo) 4 x 16-bit
     // pieces per lane) before touching TMEM; converted where it is consumed
-    uint4 rraw[8];  // float4 bits, or {hi pieces x2, lo pieces x2}
+    // float4 bits, or {hi pieces x2, lo pieces x2}; the reference binary16 mode
+    // (R16) has no lo plane, so it keeps 8 bytes per row (register pressure of
+    // the 16-warp single-MMA epilogue)
+    using RawT = typename std::conditional<R16, uint2, uint4>::type;
+    RawT rraw[8];
     if (EPI == EPI_F32_RES) {
 #pragma unroll
       for (int it = 0; it < 8; ++it) {
         const int r = it * 4 + rs;
         const size_t o = (size_t)(row0 + (r < rows ? r : 0)) * args.ldr + col;
-        if (r16res) {
+        if constexpr (R16) {  // an fp32 residual (pre-norm x32) is read where it is used
+          if (r16res) rraw[it] = *reinterpret_cast<const uint2*>(args.res_hi + o);
+        } else if (r16res) {
           const uint2 h = *reinterpret_cast<const uint2*>(args.res_hi + o);
           const uint2 l = args.res_lo ? *reinterpret_cast<const uint2*>(args.res_lo + o)
                                       : make_uint2(0u, 0u);
@@ -213,7 +219,17 @@ __device__ __forceinline__ void epi_tile_t(const GemmArgs& args, uint32_t tacc, 
       if (EPI == EPI_F32 || EPI == EPI_F32_RES) {
         if (EPI == EPI_F32_RES) {
           float2 r01, r23;
-          if (r16res) {
+          if constexpr (R16) {
+            if (r16res) {
+              const uint16_t* h = reinterpret_cast<const uint16_t*>(&rraw[it].x);
+              r01 = make_float2(load16(h, 0, FMT), load16(h, 1, FMT));
+              r23 = make_float2(load16(h, 2, FMT), load16(h, 3, FMT));
+            } else {
+              const float4 rf = *reinterpret_cast<const float4*>(args.residual + o * args.ldr + col);
+              r01 = make_float2(rf.x, rf.y);
+              r23 = make_float2(rf.z, rf.w);
+            }
+          } else if (r16res) {
             const uint16_t* h = reinterpret_cast<const uint16_t*>(&rraw[it].x);
             const uint16_t* l = reinterpret_cast<const uint16_t*>(&rraw[it].z);
             r01 = make_float2(load16(h, 0, FMT) + load16(l, 0, FMT), load16(h, 1, FMT) + load16(l, 1, FMT));
@@ -314,6 +330,19 @@ __device__ __forceinline__ void epi_dispatch(const GemmArgs& args, F&& f) {
   } else {
     f(std::integral_constant<int, FMT_BF16>{}, std::false_type{});
   }
+}
+
+// VAR pins the epilogue variant at compile time (1: binary16 reference mode,
+// 2: bf16) so a kernel only carries the registers of the variant it runs; 0
+// dispatches on the arguments.
+template <int VAR, class F>
+__device__ __forceinline__ void epi_dispatch_v(const GemmArgs& args, F&& f) {
+  if constexpr (VAR == 1)
+    f(std::integral_constant<int, FMT_F16>{}, std::true_type{});
+  else if constexpr (VAR == 2)
+    f(std::integral_constant<int, FMT_BF16>{}, std::false_type{});
+  else
+    epi_dispatch(args, f);
 }
 
 template <int BN, bool SPLIT, int EPI>
@@ -502,7 +531,7 @@ struct Gemm2Cfg {
   static_assert(STAGES >= 2, "pipeline needs at least two stages");
 };
 
-template <bool SPLIT, int EPI>
+template <bool SPLIT, int EPI, int VAR = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THREADS, 1)
     gemm2_tc_kernel(const __grid_constant__ CUtensorMap mapAh,
                     const __grid_constant__ CUtensorMap mapAl,
@@ -532,12 +561,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
   // an A block or a weight slice stream it at the same time and hit in L2; the
   // static round-robin drifted apart over long K loops) and publishes it to a
   // TRING-deep ring in both CTAs; every other role reads the ids from its ring.
-  auto ring_get = [&](int i, bool leader_release) -> int {
+  // Slot release: only the leader's MMA thread and rank 1's producer arrive on
+  // tr_empty (neither has generic global stores in flight, so the release-cluster
+  // arrive is cheap). The epilogue warps read slot i before they free tile
+  // (i+1)'s accumulator, and the producer can only publish tile i+4 into that
+  // slot after the MMAs of tile i+3 -- which needed that accumulator -- started.
+  auto ring_get = [&](int i, int release) -> int {  // release: 0 none, 1 local, 2 remote
     const int slot = i % TRING;
     mbar_wait_cluster(&tr_full[slot], (uint32_t)(i / TRING) & 1);
-    const int t = *(volatile int*)&tring[slot];
-    if (leader_release) mbar_arrive(&tr_empty[slot]);
-    else mbar_arrive_cluster(mapa_shared(&tr_empty[slot], 0));
+    const int t = tring[slot];
+    if (release == 1) mbar_arrive(&tr_empty[slot]);
+    else if (release == 2) mbar_arrive_cluster(mapa_shared(&tr_empty[slot], 0));
     return t;
   };
 
@@ -558,8 +592,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
     }
     for (int r = 0; r < TRING; ++r) {
       mbar_init(&tr_full[r], 1);
-      // leader's MMA warp + rank 1's producer + both CTAs' epilogue warps
-      mbar_init(&tr_empty[r], 2 + 2 * C::EPI_WARPS);
+      mbar_init(&tr_empty[r], 2);  // leader's MMA thread + rank 1's producer
     }
     fence_mbar_init();
   }
@@ -598,7 +631,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
           mbar_arrive(&tr_full[slot]);
           mbar_arrive_cluster(trfull_peer + 8 * slot);
         } else {
-          tile = ring_get(i, false);
+          tile = ring_get(i, 2);
         }
         if (tile < 0) {
           // the last pair to finish re-arms the counter for the next launch (every
@@ -647,7 +680,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
       uint32_t acc_phase = 0;
       const int kc = args.kchunk > 0 ? args.kchunk : kblocks;
       for (int i = 0;; ++i) {
-        if (ring_get(i, true) < 0) break;
+        if (ring_get(i, 1) < 0) break;
         for (int cb = 0; cb < kblocks; cb += kc) {  // one fresh accumulator per K chunk
           const int ce = min(kblocks, cb + kc);
           mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -691,12 +724,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THR
     const int nch = (kblocks + kc - 1) / kc;
     float* part_row =
         nch > 1 ? args.partial + (size_t)blockIdx.x * GEMM_BM * BN + (q * 32 + lane) * 4 : nullptr;
-    epi_dispatch(args, [&](auto fmt_c, auto r16_c) {
+    epi_dispatch_v<VAR>(args, [&](auto fmt_c, auto r16_c) {
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int i = 0;; ++i) {
         int tile = 0;
-        if (lane == 0) tile = ring_get(i, rank == 0);
+        if (lane == 0) tile = ring_get(i, 0);
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile < 0) break;
         int mt, nt;
