@@ -121,7 +121,7 @@ static cudaError_t run(const CUtensorMap* ah, const CUtensorMap* al, const CUten
 template <bool SPLIT, int EPI>
 static cudaError_t run2(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* bh,
                         const CUtensorMap* bl, const GemmArgs& a, int num_sms, cudaStream_t st) {
-  using C = Gemm2Cfg<SPLIT>;
+  using C = Gemm2Cfg<SPLIT, EPI>;
   // single-MMA kernels (16 epilogue warps, 96 registers) get their epilogue
   // variant fixed at compile time: the binary16 mode then needs no lo-plane
   // residual registers and does not spill in the epilogue loop

@@ -513,11 +513,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // Barriers: full[s] lives in the leader (both CTAs' TMA bytes complete on it);
 // empty[s] / tfull[a] are signalled in both CTAs by a multicast commit;
 // tempty[a] lives in the leader and counts both CTAs' epilogue warps.
-template <bool SPLIT>
+template <bool SPLIT, int EPI>
 struct Gemm2Cfg {
-  // one-MMA (non-split) tiles finish the mainloop 3x sooner, so their epilogue
-  // gets 16 warps (4 per TMEM lane quarter) instead of 8
-  static constexpr int EPI_WARPS = SPLIT ? 8 : 16;
+  // Epilogue warps vs mainloop stages (they share the 227 KB of shared memory:
+  // 4 KB of transpose buffer per epilogue warp). One-MMA (non-split) mainloops
+  // need 3x the operand bytes per MMA-cycle and, with 5 stages, waited on TMA
+  // data (ncu: their epilogue warps sat in the accumulator-full wait), so they
+  // run 8 epilogue warps and 6 stages (fp16 mode +2.6 %, bf16 +3.6 %) -- except
+  // the GELU epilogue (FFN1), whose math needs the 16 warps more than a stage.
+  static constexpr int EPI_WARPS = SPLIT ? 8 : (EPI == EPI_GELU_SPLIT ? 16 : 8);
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int EPI_BYTES = EPI_WARPS * 32 * GEMM_EPI_STRIDE * 4;
   static constexpr int NOPS = SPLIT ? 2 : 1;
@@ -532,12 +536,12 @@ struct Gemm2Cfg {
 };
 
 template <bool SPLIT, int EPI, int VAR = 0>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT>::THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT, EPI>::THREADS, 1)
     gemm2_tc_kernel(const __grid_constant__ CUtensorMap mapAh,
                     const __grid_constant__ CUtensorMap mapAl,
                     const __grid_constant__ CUtensorMap mapBh,
                     const __grid_constant__ CUtensorMap mapBl, const GemmArgs args) {
-  using C = Gemm2Cfg<SPLIT>;
+  using C = Gemm2Cfg<SPLIT, EPI>;
   constexpr int BN = 256;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
