@@ -80,16 +80,20 @@ int gemm_b_box_rows(int bn) { return gemm_uses_pair(bn) ? 128 : bn; }
 // in two halves. At config 2's K = 1024 / 4096 the error is small enough for
 // the parity gate and the chunk drains would cost ~1.5 % (measured). MFG_KCHUNK=E chunks every E elements whenever
 // K > E; MFG_KCHUNK=0 disables. Returns k-blocks per chunk (0 = no chunking).
-int gemm_kchunk_blocks(int K) {
+int gemm_kchunk_blocks(int K, bool fine) {
   static const int env = [] {
     const char* e = getenv("MFG_KCHUNK");
     return e ? atoi(e) : -1;
   }();
   int elems = env;
   // default: K > 4096 in 2048-K chunks; 2048 < K <= 4096 in two halves only when
-  // K is not a power of two (XLM-R XL's 2560: measured at no cost, parity 2.5x)
+  // K is not a power of two (XLM-R XL's 2560: measured at no cost, parity 2.5x).
+  // `fine` (split-operand GEMMs of models narrower than 1024, whose GEMMs are
+  // cheap): 128-K chunks -- config 1's std-0.25 fixture model goes from 5.0e-4
+  // to 2.1e-4 max |delta| against the reference
   if (env < 0)
-    elems = K > 4096 ? 2048 : (K > 2048 && (K & (K - 1)) != 0) ? (K / 2 + 63) / 64 * 64 : 0;
+    elems = fine ? 128
+                 : K > 4096 ? 2048 : (K > 2048 && (K & (K - 1)) != 0) ? (K / 2 + 63) / 64 * 64 : 0;
   if (elems <= 0 || K <= elems) return 0;
   return elems / GEMM_BK > 0 ? elems / GEMM_BK : 1;
 }

@@ -92,7 +92,7 @@ int gemm_pick_bn(int n_pad);
 // rows that kernel expects (each CTA of a pair loads half of the N tile).
 bool gemm_uses_pair(int bn);
 int gemm_b_box_rows(int bn);
-int gemm_kchunk_blocks(int K);          // GemmArgs::kchunk for a GEMM of depth K
+int gemm_kchunk_blocks(int K, bool fine = false);  // GemmArgs::kchunk for a GEMM of depth K
 size_t gemm_partial_floats(int num_sms);  // GemmArgs::partial workspace size
 // nsplit: 1 = one MMA per k-step (hi only), 2 = hi/lo pieces, 3 MMAs per k-step.
 cudaError_t launch_gemm(const CUtensorMap* ah, const CUtensorMap* al, const CUtensorMap* bh,

@@ -193,6 +193,10 @@ struct mfg_ctx {
   int* tile_ctr = nullptr;     // CTA-pair GEMM tile counter + finished-pair count (self-resetting)
   bool dyn_tiles = !(getenv("MFG_TILE_DYN") && getenv("MFG_TILE_DYN")[0] == '0');  // A/B switch
 
+  // split-operand (fp32-parity / bf16x3) GEMMs of models narrower than 1024 restart
+  // the accumulator every 128 K (gemm_kchunk_blocks)
+  bool fine_kchunk() const { return split && d < 1024; }
+
   void apply_l2_window(cudaStream_t s) {
     if (!part_persist || !s) return;
     int max_win = 0;
@@ -516,7 +520,8 @@ struct mfg_ctx {
     // streams those lines were evicted to DRAM between the drain and the next
     // read (ncu, config 5: ~60 GB of extra DRAM traffic per layer). Pin the
     // buffer in L2 as a persisting access-policy window on the launch stream.
-    part_persist = (gemm_kchunk_blocks(dp) > 0 || gemm_kchunk_blocks(fp) > 0) &&
+    part_persist = (gemm_kchunk_blocks(dp, fine_kchunk()) > 0 ||
+                    gemm_kchunk_blocks(fp, fine_kchunk()) > 0) &&
                    !(getenv("MFG_L2_PERSIST") && getenv("MFG_L2_PERSIST")[0] == '0');
     if (part_persist) {
       int max_persist = 0;
@@ -593,7 +598,7 @@ struct mfg_ctx {
     g.K = w.Kpad;
     g.bias = w.bias;
     g.alpha = w.alpha;
-    g.kchunk = gemm_kchunk_blocks(w.Kpad);
+    g.kchunk = gemm_kchunk_blocks(w.Kpad, fine_kchunk());
     g.partial = gemm_part;
     g.tile_ctr = dyn_tiles ? tile_ctr : nullptr;
     g.residual = res;
