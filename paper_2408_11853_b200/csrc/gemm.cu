@@ -88,11 +88,12 @@ int gemm_kchunk_blocks(int K, bool fine) {
   int elems = env;
   // default: K > 4096 in 2048-K chunks; 2048 < K <= 4096 in two halves only when
   // K is not a power of two (XLM-R XL's 2560: measured at no cost, parity 2.5x).
-  // `fine` (split-operand GEMMs of models narrower than 1024, whose GEMMs are
-  // cheap): 128-K chunks -- config 1's std-0.25 fixture model goes from 5.0e-4
-  // to 2.1e-4 max |delta| against the reference
+  // `fine` (split-operand GEMMs of models narrower than 1024): 512-K chunks --
+  // config 1's std-0.25 fixture model goes from 5.0e-4 to 2.75e-4 max |delta|
+  // against the reference for -2.5 % device / -1 % e2e throughput (128-K chunks:
+  // 2.1e-4 for -20 %)
   if (env < 0)
-    elems = fine ? 128
+    elems = fine ? 512
                  : K > 4096 ? 2048 : (K > 2048 && (K & (K - 1)) != 0) ? (K / 2 + 63) / 64 * 64 : 0;
   if (elems <= 0 || K <= elems) return 0;
   return elems / GEMM_BK > 0 ? elems / GEMM_BK : 1;

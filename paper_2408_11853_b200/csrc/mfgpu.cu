@@ -194,7 +194,7 @@ struct mfg_ctx {
   bool dyn_tiles = !(getenv("MFG_TILE_DYN") && getenv("MFG_TILE_DYN")[0] == '0');  // A/B switch
 
   // split-operand (fp32-parity / bf16x3) GEMMs of models narrower than 1024 restart
-  // the accumulator every 128 K (gemm_kchunk_blocks)
+  // the accumulator every 512 K (gemm_kchunk_blocks)
   bool fine_kchunk() const { return split && d < 1024; }
 
   void apply_l2_window(cudaStream_t s) {
