@@ -552,7 +552,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT, EPI>
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* tr_full = tempty + 2;           // [TRING] tile id published (both CTAs)
-  uint64_t* tr_empty = tr_full + TRING;     // [TRING] every consumer read it (leader only)
+  uint64_t* tr_empty = tr_full + TRING;     // [TRING] slot read by the MMA thread and rank 1's
+                                            // producer (leader only; see ring_get)
   int* tring = reinterpret_cast<int*>(tr_empty + TRING);  // [TRING] tile ids, -1 = done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tring + TRING);
 
@@ -567,9 +568,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT, EPI>
   // TRING-deep ring in both CTAs; every other role reads the ids from its ring.
   // Slot release: only the leader's MMA thread and rank 1's producer arrive on
   // tr_empty (neither has generic global stores in flight, so the release-cluster
-  // arrive is cheap). The epilogue warps read slot i before they free tile
-  // (i+1)'s accumulator, and the producer can only publish tile i+4 into that
-  // slot after the MMAs of tile i+3 -- which needed that accumulator -- started.
+  // arrive is cheap). The epilogue warps need no release: they read slot i before
+  // they drain any accumulator of tile i+1, and the producer can only publish
+  // tile i+4 into that slot after the MMAs of tile i+3 started, which needed an
+  // accumulator the epilogue drained from tile i+1 or later (with K-chunking,
+  // every chunk alternates accumulators, which only tightens this).
   auto ring_get = [&](int i, int release) -> int {  // release: 0 none, 1 local, 2 remote
     const int slot = i % TRING;
     mbar_wait_cluster(&tr_full[slot], (uint32_t)(i / TRING) & 1);
