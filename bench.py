@@ -205,6 +205,20 @@ def cpu_info():
     return {"cpu": model, "cpu_count": os.cpu_count(), "affinity": avail}
 
 
+def all_host_threads():
+    """The reference arm uses every host thread it can (torchrun exports
+    OMP_NUM_THREADS=1 to its workers, which would pin numpy's BLAS to one)."""
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count() or 1
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=n, user_api="blas")
+    except Exception:
+        return None
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -267,6 +281,7 @@ def cpu_baseline(cfg, path, vocab, n_records):
     host cores (1 discarded record, then the sample once, like the reference
     bench's discard + timed passes, `cli.py:309-315`)."""
     from oracle import fixtures as fx
+    _limits = all_host_threads()  # noqa: F841
     ref = CpuReference(cfg, path, vocab)
     lines = workload_lines(cfg, n_records + 1, fx.TEXT_SEED + 777)
     ref.score(lines[:1])
@@ -339,6 +354,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     from oracle import fixtures as fx
+    _limits = all_host_threads()  # noqa: F841 - kept alive for the run
     man, path, vocab = prepare_model(args.config, 0, 1, lambda: None)
     ref = CpuReference(args.config, path, vocab)
     per_step = REF_PER_STEP[args.config]
