@@ -130,19 +130,32 @@ __device__ __forceinline__ uint32_t h22u(__half2 h) { return *reinterpret_cast<c
 // once to binary16 is the correctly rounded binary16 sum, so this equals
 // round16(round16(acc) + b)); with a binary16 residual and output the residual
 // sum is one more __hadd2.
-template <int BN, int EPI, int NSUB, int FMT, bool R16>
+//
+// CW (transpose width, 32 or 16 columns): each warp still owns the same 32-column
+// chunks (the K-chunk partial sums are per warp), processed CW columns at a
+// time; CW = 16 halves the transpose buffer (2 KB per warp), which buys the
+// single-MMA kernels a sixth mainloop stage with all 16 epilogue warps.
+template <int BN, int EPI, int NSUB, int FMT, bool R16, int CW = 32>
 __device__ __forceinline__ void epi_tile_t(const GemmArgs& args, uint32_t tacc, int row0, int rows,
                                            int n0, int half, float* buf, int lane,
                                            const float* part_row = nullptr) {
-  const int cg = lane & 7;       // transposed phase: 4 columns 4*cg..4*cg+3
-  const int rs = lane >> 3;      // row sub-index 0..3
+  static_assert(CW == 32 || CW == 16, "transpose width");
+  constexpr int NQ = CW / 4;        // float4 chunks per transposed row
+  constexpr int RPI = 32 / NQ;      // rows per pass of the transposed phase (4 or 8)
+  constexpr int NIT = 32 / RPI;     // passes (8 or 4)
+  const int cg = lane % NQ;         // transposed phase: 4 columns 4*cg..4*cg+3
+  const int rs = lane / NQ;         // row sub-index 0..RPI-1
+  // 16-byte chunk swizzle of a transposed row (conflict-free writes and reads)
+  auto swz = [](int r) { return CW == 32 ? (r & 7) : ((r >> 1) & 3); };
   const bool r16res = EPI == EPI_F32_RES && args.res_hi != nullptr;
   const bool h16 = R16 && r16res && args.res_lo == nullptr && args.out16 != nullptr;
   constexpr bool SPLIT_OUT = EPI == EPI_GELU_SPLIT || EPI == EPI_TANH_SPLIT || EPI == EPI_SPLIT;
   float amax = 0.f;  // largest |output| (fp16 overflow flag, split epilogues)
   uint32_t hinf = 0;  // R16 EPI_SPLIT: bit 15/31 set when a binary16 output is inf
 #pragma unroll 1
-  for (int c = half * 32; c < BN; c += 32 * NSUB) {
+  for (int c32 = half * 32; c32 < BN; c32 += 32 * NSUB)
+#pragma unroll 1
+  for (int c = c32; c < c32 + 32; c += CW) {
     const int col = n0 + c + 4 * cg;
     // prefetch this chunk's residual (8 x float4, or 8 x (hi, lo) 4 x 16-bit
     // pieces per lane) before touching TMEM; converted where it is consumed
@@ -150,11 +163,11 @@ __device__ __forceinline__ void epi_tile_t(const GemmArgs& args, uint32_t tacc, 
     // (R16) has no lo plane, so it keeps 8 bytes per row (register pressure of
     // the 16-warp single-MMA epilogue)
     using RawT = typename std::conditional<R16, uint2, uint4>::type;
-    RawT rraw[8];
+    RawT rraw[NIT];
     if (EPI == EPI_F32_RES) {
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const int r = it * 4 + rs;
+      for (int it = 0; it < NIT; ++it) {
+        const int r = it * RPI + rs;
         const size_t o = (size_t)(row0 + (r < rows ? r : 0)) * args.ldr + col;
         if constexpr (R16) {  // an fp32 residual (pre-norm x32) is read where it is used
           if (r16res) rraw[it] = *reinterpret_cast<const uint2*>(args.res_hi + o);
@@ -168,18 +181,19 @@ __device__ __forceinline__ void epi_tile_t(const GemmArgs& args, uint32_t tacc, 
         }
       }
     }
-    float v[32];
-    tmem_ld_32x32(tacc + c, v);
-    if (part_row) {  // earlier K chunks of this tile (this thread's row, columns c..c+31)
+    float v[CW];
+    if constexpr (CW == 32) tmem_ld_32x32(tacc + c, v);
+    else tmem_ld_32x16(tacc + c, v);
+    if (part_row) {  // earlier K chunks of this tile (this thread's row, columns c..c+CW-1)
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) {
+      for (int i = 0; i < CW; i += 4) {
         const float4 pp = *reinterpret_cast<const float4*>(part_row + (c + i) * GEMM_BM);
         v[i] += pp.x, v[i + 1] += pp.y, v[i + 2] += pp.z, v[i + 3] += pp.w;
       }
     }
 #pragma unroll
-    for (int i = 0; i < 32; i += 4)
-      *reinterpret_cast<float4*>(buf + lane * GEMM_EPI_STRIDE + (((i >> 2) ^ (lane & 7)) << 2)) =
+    for (int i = 0; i < CW; i += 4)
+      *reinterpret_cast<float4*>(buf + lane * CW + (((i >> 2) ^ swz(lane)) << 2)) =
           make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
     __syncwarp();
     const float4 b = *reinterpret_cast<const float4*>(args.bias + col);
@@ -188,9 +202,8 @@ __device__ __forceinline__ void epi_tile_t(const GemmArgs& args, uint32_t tacc, 
                                  : make_float4(1.f, 1.f, 1.f, 1.f);
     const __half2 bh01 = __floats2half2_rn(b.x, b.y), bh23 = __floats2half2_rn(b.z, b.w);
     auto row = [&](int it) {
-      const int r = it * 4 + rs;
-      const float4 s4 =
-          *reinterpret_cast<const float4*>(buf + r * GEMM_EPI_STRIDE + ((cg ^ (r & 7)) << 2));
+      const int r = it * RPI + rs;
+      const float4 s4 = *reinterpret_cast<const float4*>(buf + r * CW + ((cg ^ swz(r)) << 2));
       const size_t o = (size_t)(row0 + r);
       float2 x01, x23;
       if (R16) {
@@ -287,8 +300,8 @@ __device__ __forceinline__ void epi_tile_t(const GemmArgs& args, uint32_t tacc, 
       }
     };
 #pragma unroll
-    for (int it = 0; it < 8; ++it)
-      if (it * 4 + rs < rows) row(it);
+    for (int it = 0; it < NIT; ++it)
+      if (it * RPI + rs < rows) row(it);
     __syncwarp();
   }
   if (SPLIT_OUT && FMT == FMT_F16 && args.ovf && (amax >= 65520.f || (hinf & 0x80008000u)))
@@ -518,12 +531,16 @@ struct Gemm2Cfg {
   // Epilogue warps vs mainloop stages (they share the 227 KB of shared memory:
   // 4 KB of transpose buffer per epilogue warp). One-MMA (non-split) mainloops
   // need 3x the operand bytes per MMA-cycle and, with 5 stages, waited on TMA
-  // data (ncu: their epilogue warps sat in the accumulator-full wait), so they
-  // run 8 epilogue warps and 6 stages (fp16 mode +2.6 %, bf16 +3.6 %) -- except
-  // the GELU epilogue (FFN1), whose math needs the 16 warps more than a stage.
-  static constexpr int EPI_WARPS = SPLIT ? 8 : (EPI == EPI_GELU_SPLIT ? 16 : 8);
+  // data (ncu: their epilogue warps sat in the accumulator-full wait). Measured
+  // per epilogue (same-box A/B, profiles/gemm_raster_r03.txt): 8 warps with the
+  // 32-column transpose and 6 stages for the plain / residual / split epilogues;
+  // 16 warps transposing 16 columns at a time (2 KB per warp, still 6 stages)
+  // for GELU (FFN1), whose math needs the warps.
+  static constexpr bool WIDE = !SPLIT && EPI == EPI_GELU_SPLIT;
+  static constexpr int EPI_WARPS = WIDE ? 16 : 8;
+  static constexpr int EPI_CW = WIDE ? 16 : 32;  // transpose width (epi_tile_t)
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
-  static constexpr int EPI_BYTES = EPI_WARPS * 32 * GEMM_EPI_STRIDE * 4;
+  static constexpr int EPI_BYTES = EPI_WARPS * 32 * EPI_CW * 4;
   static constexpr int NOPS = SPLIT ? 2 : 1;
   static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;  // this CTA's 128 rows
   static constexpr int B_BYTES = 128 * GEMM_BK * 2;      // this CTA's half of BN = 256
@@ -725,7 +742,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT, EPI>
     const int ew = warp - 4;       // 0..EPI_WARPS-1
     const int q = warp & 3;        // TMEM lane quarter == 32-row block of this CTA's half tile
     const int half = ew >> 2;      // which 32-column chunks (every EPI_WARPS/4-th) it owns
-    float* buf = epi_buf + ew * 32 * GEMM_EPI_STRIDE;
+    float* buf = epi_buf + ew * 32 * C::EPI_CW;
     const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
     const int kc = args.kchunk > 0 ? args.kchunk : kblocks;
     const int nch = (kblocks + kc - 1) / kc;
@@ -752,7 +769,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<SPLIT, EPI>
           if (ch + 1 < nch)
             drain_chunk<BN, C::EPI_WARPS / 4>(tacc, part_row, ch == 0, half);
           else if (rows > 0)
-            epi_tile_t<BN, EPI, C::EPI_WARPS / 4, decltype(fmt_c)::value, decltype(r16_c)::value>(
+            epi_tile_t<BN, EPI, C::EPI_WARPS / 4, decltype(fmt_c)::value, decltype(r16_c)::value,
+                       C::EPI_CW>(
                 args, tacc, row0, rows, n0, half, buf, lane, part_row);
           tc_fence_before();
           __syncwarp();
