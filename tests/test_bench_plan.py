@@ -35,3 +35,28 @@ def test_rank_steps_cover_every_record_once(world):
     assert np.array_equal(allpos, np.arange(n))
     if world > 1:
         assert max(loads) / (sum(loads) / world) < 1.15
+
+
+def test_reference_arm_prints_one_line(tmp_path):
+    """`bench.py --impl reference` (the driver's reference arm): the reference's
+    own CPU Evaluator (baseline/_ref when installed, else the oracle port) on the
+    config's workload; one JSON line with impl, cpu_baseline and a zero-copy e2e."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+    env = dict(os.environ, MFG_BENCH_DIR=str(tmp_path))
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config", "1",
+                        "--steps", "2", "--warmup", "3"], capture_output=True, text=True,
+                       timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "segments/s"
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
