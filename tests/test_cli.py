@@ -125,3 +125,18 @@ def test_stdin_stream_bad_line_index_matches_list_path(tiny_factory):
     r = cli("-m", fix.model, "-v", fix.vocab, "--stdin", stdin="".join(l + "\n" for l in lines))
     assert r.returncode == 2 and r.stdout == ""
     assert "line 29876: expected 2 tab-separated columns, got 1" in r.stderr
+
+
+@pytest.mark.gpu
+def test_eight_ranks_score_bitwise_like_one(tiny_factory):
+    """scores at 1 and 8 ranks are identical (here 8 ranks share the
+    test box's GPU; whole mini-batches are LPT-assigned, no collective on the data
+    path). 3000 records = 3 windows of 128 x 8, more mini-batches than ranks."""
+    fix = tiny_factory("comet-qe", "pre", 77)
+    lines = fx.fixture_tsv_lines("comet-qe", 3000, seed=8)
+    tsv = "".join(l + "\n" for l in lines)
+    base = ["-m", fix.model, "-v", fix.vocab, "--quiet", "--precision", "9", "--max-tokens", "32768"]
+    one = cli(*base, "--stdin", stdin=tsv)
+    eight = _multi(*base, "--stdin", "--gpus", "8", stdin=tsv)
+    assert one.returncode == 0 and eight.returncode == 0, eight.stderr[-2000:]
+    assert len(one.stdout.splitlines()) == 3000 and eight.stdout == one.stdout
