@@ -177,15 +177,14 @@ cudaError_t launch_gemm(const CUtensorMap* ah, const CUtensorMap* al, const CUte
                         const CUtensorMap* bl, int bn, int nsplit, int epi, const GemmArgs& a_in,
                         int num_sms, cudaStream_t st) {
   if (a_in.K % GEMM_BK != 0 || a_in.N % bn != 0) return cudaErrorInvalidValue;
-  // Tile raster (profiles/gemm_raster_r03.txt, measured per GEMM with ncu):
-  //  * narrow (N <= 1024: config-2 O-proj, FFN2): groups of 4 M-blocks M-fastest —
-  //    FFN2 DRAM 11.3 -> 8.2 GB per launch (algorithmic 5.2 GB), 3.7 % faster alone;
-  //  * wide GEMMs whose weight does not stay L2-resident (> 48 MB of pieces, >= 16
-  //    N-tiles: XLM-R XL QKV 79 MB, FFN1 105 MB): groups of 16 M-blocks, so a few
-  //    N-tiles' weights are shared by 16 concurrent M-blocks instead of every
-  //    M-block sweeping the whole weight — FFN1 DRAM read 88 -> 65 GB, -5.6 %;
-  //  * otherwise N-fastest (an M-block's A is shared by its concurrent N-tiles).
-  // MFG_GEMM_GROUP=G forces G for every GEMM.
+  // Tile raster (profiles/gemm_raster_r03.txt, measured per GEMM with ncu, with
+  // the dynamic tile hand-out): N-fastest (an M-block's A is shared by its
+  // concurrent N-tiles) except for wide GEMMs whose weight does not stay
+  // L2-resident (> 48 MB of pieces, >= 16 N-tiles: XLM-R XL QKV 79 MB, FFN1
+  // 105 MB), which walk groups of 8 M-blocks so a few N-tiles' weights are
+  // shared by 8 concurrent M-blocks -- XL FFN1 DRAM read 98 -> 22 GB, -14 %.
+  // (Config 2's FFN2 was grouped by 4 under the static schedule; with dynamic
+  // tiles N-fastest reads less: 5.8 vs 6.3 GB.) MFG_GEMM_GROUP=G forces G.
   static const int group_env = [] {
     const char* e = getenv("MFG_GEMM_GROUP");
     return e ? atoi(e) : -1;
@@ -193,9 +192,7 @@ cudaError_t launch_gemm(const CUtensorMap* ah, const CUtensorMap* al, const CUte
   GemmArgs a = a_in;
   const int num_n = a.N / bn;
   const double w_bytes = (double)a.N * a.K * (nsplit == 2 ? 4 : 2);
-  int group = 0;
-  if (gemm_uses_pair(bn) && num_n <= 4) group = 4;
-  else if (gemm_uses_pair(bn) && num_n >= 16 && w_bytes > 48e6) group = 16;
+  const int group = gemm_uses_pair(bn) && num_n >= 16 && w_bytes > 48e6 ? 8 : 0;
   a.group_m = group_env >= 0 ? group_env : group;
   const bool split = nsplit == 2;
   if (!gemm_uses_pair(bn) || a.partial == nullptr) a.kchunk = 0;
